@@ -1,0 +1,157 @@
+/*
+ * hobi.h -- C ABI of the B200-native HOBI-PB boundary-integral hot path.
+ *
+ * The reference (arXiv 1301.5914 restated as the Python package `pbbem`, see
+ * SURVEY.md) has no native boundary: its hot path is the Python operator
+ * protocol in /root/reference/pkg/src/pbbem/solver.py.  Each entry point below
+ * replaces one reference interface, cited as file:line relative to that
+ * package.  Plain pointers and sizes only; every array is C-contiguous
+ * float64 / int64 in the reference's layout; all pointers are HOST pointers
+ * unless the name ends in `_device`.  The library owns its device buffers
+ * for the lifetime of a context.  Contexts are not thread-safe.
+ *
+ * Status codes map 1:1 to the reference's exception types (hobi_last_error()
+ * returns the message text, formatted like the reference's).
+ */
+#ifndef HOBI_H
+#define HOBI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HOBI_ABI_VERSION 1
+
+enum hobi_status {
+  HOBI_OK = 0,
+  HOBI_ERR_VALUE = 1,          /* ValueError (solver.py:373-374, 381-382, 493-494)          */
+  HOBI_ERR_DEGENERATE_ARC = 2, /* geometry.DegenerateArcError ("face f: ...", solver.py:205) */
+  HOBI_ERR_SINGULARITY = 3,    /* kernels.SingularityError (kernels.py:167-172)             */
+  HOBI_ERR_NONCONVERGENCE = 4, /* solver.GmresNonConvergence (solver.py:521-526)             */
+  HOBI_ERR_CUDA = 5,           /* device / driver failure                                    */
+  HOBI_ERR_NCCL = 6,           /* collective failure                                         */
+  HOBI_ERR_STATE = 7           /* misuse of the API (wrong order of calls, bad handle)       */
+};
+
+typedef struct hobi_ctx hobi_ctx;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* hobi_last_error(void);
+int hobi_abi_version(void);
+int hobi_device_count(int* count);
+
+/*
+ * Build every discretisation cache on `device`: curved cubic nodes for the
+ * three rotations of every face, frames at the regular and Duffy points,
+ * incident-pair tables.  Replaces solver.discretize (solver.py:165-266) for
+ * scheme "hobi" (the mesh must already have passed FlatMesh.validate,
+ * mesh.py:50-75, which the host wrapper calls first).
+ *   vertices, normals : (nv, 3)      faces : (nf, 3) int64
+ *   reg_pts (nq, 2), reg_wts (nq), reg_shape (3, nq, 10): N, dN/dr, dN/ds
+ *   (quadrature.py:68-87, geometry.py:197-205); duf_* likewise for the
+ *   Duffy rule (quadrature.py:101-116).  nq <= 16, nd <= 64.
+ * Fails with HOBI_ERR_DEGENERATE_ARC at the first failing face in face
+ * order, rotations 0,1,2 (solver.py:198-206).
+ */
+int hobi_create(int device, const double* vertices, const double* normals, int64_t nv,
+                const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
+                const double* reg_pts, const double* reg_wts, const double* reg_shape, int nq,
+                const double* duf_pts, const double* duf_wts, const double* duf_shape, int nd,
+                hobi_ctx** out);
+
+/* LOBI (flat centroid) discretisation: solver.py:177-186.  No rules needed. */
+int hobi_create_lobi(int device, const double* vertices, const double* normals, int64_t nv,
+                     const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
+                     hobi_ctx** out);
+
+/* Release the context: _Operator.close (solver.py:461-466). */
+int hobi_destroy(hobi_ctx* ctx);
+
+/* n_collocation (solver.py:142-144): N_v for hobi, N_f for lobi. */
+int hobi_size(hobi_ctx* ctx, int64_t* n_colloc, int64_t* n_sources);
+
+/*
+ * One operator application u -> A u over HOST buffers of length 2*n_colloc,
+ * including both copies: _Operator.__call__ / matvec_hobi / matvec_lobi
+ * (solver.py:447-459, 370-390).  Under a communicator (hobi_comm_init) every
+ * rank passes the full u and receives the full A u.
+ */
+int hobi_matvec(hobi_ctx* ctx, const double* u, double* out);
+/* Same on device pointers already resident in HBM (the ctx's stream). */
+int hobi_matvec_device(hobi_ctx* ctx, const double* u_device, double* out_device);
+/*
+ * Rows [lo, hi) of both blocks only: _apply_range (solver.py:278-367).
+ * out_phi, out_dphi have hi-lo entries each.  Results are bitwise
+ * independent of how [0, n) is split (solver.py:12-17).
+ */
+int hobi_matvec_rows(hobi_ctx* ctx, const double* u, int64_t lo, int64_t hi, double* out_phi,
+                     double* out_dphi);
+
+/* b = (S1, S2)/eps1 at the collocation points: assemble_rhs (solver.py:393-402)
+ * over source_terms_at (kernels.py:159-178).  b has 2*n_colloc entries. */
+int hobi_rhs(hobi_ctx* ctx, const double* qpos, const double* q, int64_t nc, double* b);
+
+/* Reaction-field energy in kcal/mol: solvation_energy (solver.py:581-614). */
+int hobi_energy(hobi_ctx* ctx, const double* qpos, const double* q, int64_t nc, const double* phi,
+                const double* dphi, double* energy);
+
+/*
+ * Device-resident restarted GMRES with MGS + Givens and true-residual restarts:
+ * gmres_solve (solver.py:484-560) applied to this context's operator.  x has
+ * 2*n_colloc entries.  On HOBI_ERR_NONCONVERGENCE `best` holds the best
+ * relative residual (GmresNonConvergence.best_residual).
+ */
+int hobi_gmres(hobi_ctx* ctx, const double* b, double tol, int restart, int max_it, double* x,
+               int* iterations, double* residual, double* best, int* matvecs);
+
+/*
+ * The same GMRES on an arbitrary operator supplied as a host callback
+ * (gmres_solve accepts any callable, solver.py:484).  `apply` receives host
+ * arrays of length n and returns 0 on success.
+ */
+typedef int (*hobi_apply_fn)(void* user, const double* in, double* out, int64_t n);
+int hobi_gmres_host_operator(int device, int64_t n, hobi_apply_fn apply, void* user,
+                             const double* b, double tol, int restart, int max_it, double* x,
+                             int* iterations, double* residual, double* best, int* matvecs);
+
+/* Copy device caches back in the reference's layout (DiscretizedProblem fields,
+ * solver.py:122-140).  Any pointer may be NULL. */
+int hobi_export_caches(hobi_ctx* ctx, double* reg_pos, double* reg_nrm, double* reg_w,
+                       double* duf_pos, double* duf_nrm, double* duf_w, int64_t* pair_vertex,
+                       int64_t* pair_face, int64_t* pair_gverts, int64_t* pair_starts);
+
+/* K1..K4 of kernels.kernel_values_d (kernels.py:99-130) on the device, for n
+ * displacement/normal triples (n,3); k has shape (4, n).  Test hook. */
+int hobi_kernel_values(int device, const double* d, const double* nx, const double* ny, int64_t n,
+                       double eps1, double eps2, double kappa, double* k);
+
+/*
+ * Multi-GPU row split: one process per GPU.  Rank r owns rows
+ * partition_targets(n_colloc, nranks)[r] (solver.py:405-418); each matvec
+ * ends with one ncclAllGather of the owned rows over NVLink.
+ * hobi_comm_unique_id is called on rank 0; the 128 bytes are broadcast by the
+ * host (torch.distributed) and passed to hobi_comm_init on every rank.
+ */
+int hobi_comm_unique_id(unsigned char id[128]);
+int hobi_comm_init(hobi_ctx* ctx, const unsigned char id[128], int nranks, int rank);
+/* Single-GPU emulation of an nranks-way split (same buffers, same gather
+ * layout and permutation kernel, no NCCL): for determinism tests. */
+int hobi_emulate_ranks(hobi_ctx* ctx, int nranks);
+
+/* Instrumentation: device time of the all-pairs sweep kernel (CUDA events on
+ * the launching stream) accumulated since the last reset, its launch count,
+ * and the count of every kernel this library launched. */
+int hobi_timing_reset(hobi_ctx* ctx);
+int hobi_timing(hobi_ctx* ctx, double* sweep_ms, int64_t* sweep_launches, int64_t* all_launches);
+/* Regular pairs per full matvec (N_v x N_f x nq for hobi), for throughput. */
+int hobi_pairs_per_matvec(hobi_ctx* ctx, double* pairs);
+
+/* DFMA throughput probe (FP64 roofline denominator), TFLOP/s over ~`ms` ms. */
+int hobi_probe_fp64_tflops(int device, double ms, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOBI_H */

@@ -1,0 +1,41 @@
+"""B200-native HOBI-PB: the dense boundary-integral matvec of arXiv 1301.5914
+and everything around it on the device (geometry, singular swap, sources,
+GMRES, energy, NCCL row split), behind the reference package's Python API
+(``pbbem``).  Kernels: ``csrc/`` -> ``libhobi.so`` (sm_100a);
+C ABI: ``include/hobi.h``.
+"""
+
+from .mesh import ChargeSystem, FlatMesh, MeshFormatError, MeshValidationError, icosahedral_sphere
+from .physics import FOUR_PI, KCAL_MOL_PER_E2_ANG, PhysicalParams, SingularityError
+from .quadrature import TriangleRule, duffy_rule, gauss_radau_rule
+from .solver import (
+    DegenerateArcError,
+    DiscretizedProblem,
+    GmresNonConvergence,
+    GpuOperator,
+    SolverConfig,
+    SurfaceSolution,
+    apply_rows,
+    assemble_rhs,
+    convergence_order,
+    discretize,
+    gmres_solve,
+    make_operator,
+    matvec_hobi,
+    matvec_lobi,
+    partition_targets,
+    solvation_energy,
+    solve,
+    surface_potential_error,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ChargeSystem", "DegenerateArcError", "DiscretizedProblem", "FOUR_PI", "FlatMesh",
+    "GmresNonConvergence", "GpuOperator", "KCAL_MOL_PER_E2_ANG", "MeshFormatError",
+    "MeshValidationError", "PhysicalParams", "SingularityError", "SolverConfig", "SurfaceSolution",
+    "TriangleRule", "apply_rows", "assemble_rhs", "convergence_order", "discretize", "duffy_rule",
+    "gauss_radau_rule", "gmres_solve", "icosahedral_sphere", "make_operator", "matvec_hobi",
+    "matvec_lobi", "partition_targets", "solvation_energy", "solve", "surface_potential_error",
+]

@@ -1,0 +1,630 @@
+// C ABI (include/hobi.h): context lifecycle, host-side pair tables, the
+// operator entry points, GMRES drivers and the NCCL row-gather.
+//
+// Reference mapping (paths relative to /root/reference/pkg/src/pbbem):
+//   hobi_create        <- solver.discretize            solver.py:165-266
+//   hobi_matvec*       <- _Operator.__call__/_apply_range solver.py:447-459, 278-367
+//   hobi_rhs           <- assemble_rhs                 solver.py:393-402
+//   hobi_gmres         <- gmres_solve                  solver.py:484-560
+//   hobi_energy        <- solvation_energy             solver.py:581-614
+//   hobi_comm_*        <- the fork-pool row split      solver.py:405-459
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hobi_internal.cuh"
+
+namespace hobi {
+
+static thread_local std::string g_last_error;
+
+void set_error(int status, const std::string& msg) {
+  (void)status;
+  g_last_error = msg;
+}
+
+int fail(int status, const std::string& msg) {
+  set_error(status, msg);
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(HOBI_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                                 cudaGetErrorString(e) + ") in " + what);
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time from the process (torch loads libnccl.so.2) so
+// the library has no link-time dependency and single-GPU use never needs it.
+
+namespace nccl {
+typedef struct {
+  char internal[128];
+} UniqueId;
+typedef int (*GetUniqueIdFn)(UniqueId*);
+typedef int (*CommInitRankFn)(void**, int, UniqueId, int);
+typedef int (*AllGatherFn)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef int (*CommDestroyFn)(void*);
+typedef const char* (*GetErrorStringFn)(int);
+constexpr int kFloat64 = 8;  // ncclFloat64
+
+struct Api {
+  bool loaded = false;
+  GetUniqueIdFn get_unique_id = nullptr;
+  CommInitRankFn init_rank = nullptr;
+  AllGatherFn all_gather = nullptr;
+  CommDestroyFn destroy = nullptr;
+  GetErrorStringFn err = nullptr;
+};
+
+static Api& api() {
+  static Api a;
+  if (a.loaded) return a;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  void* h = nullptr;
+  for (const char* n : names)
+    if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return a;
+  a.get_unique_id = (GetUniqueIdFn)dlsym(h, "ncclGetUniqueId");
+  a.init_rank = (CommInitRankFn)dlsym(h, "ncclCommInitRank");
+  a.all_gather = (AllGatherFn)dlsym(h, "ncclAllGather");
+  a.destroy = (CommDestroyFn)dlsym(h, "ncclCommDestroy");
+  a.err = (GetErrorStringFn)dlsym(h, "ncclGetErrorString");
+  a.loaded = a.get_unique_id && a.init_rank && a.all_gather && a.destroy;
+  return a;
+}
+
+static int check(int r, const char* what) {
+  if (r == 0) return 0;
+  const char* s = api().err ? api().err(r) : "unknown";
+  return fail(HOBI_ERR_NCCL, std::string("NCCL error in ") + what + ": " + s);
+}
+}  // namespace nccl
+
+int comm_allgather(hobi_ctx* c) {
+  auto& a = nccl::api();
+  return nccl::check(a.all_gather(c->gather_send.p, c->gather_recv.p, (size_t)(2 * c->gather_m),
+                                  nccl::kFloat64, c->comm.nccl, c->stream),
+                     "ncclAllGather");
+}
+
+static void row_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* hi) {
+  int64_t base = n / nranks, extra = n % nranks;
+  *lo = rank * base + std::min<int64_t>(rank, extra);
+  *hi = *lo + base + (rank < extra ? 1 : 0);
+}
+
+static int setup_gather(hobi_ctx* c, int nranks) {
+  c->gather_m = (c->nt + nranks - 1) / nranks;
+  if (c->gather_send.alloc(2 * c->gather_m) || c->gather_recv.alloc((size_t)nranks * 2 * c->gather_m))
+    return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemset(c->gather_recv.p, 0, (size_t)nranks * 2 * c->gather_m * sizeof(double)));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// source-group partition: a function of the problem size only (never of the
+// row split), chosen so an 8-way split still fills 148 SMs several times.
+
+static void choose_groups(hobi_ctx* c) {
+  c->n_src_tiles = (int)(c->ns_pad / kSrcTile);
+  const int64_t rows8 = (c->nt + 7) / 8;
+  const int64_t tiles8 = std::max<int64_t>(1, (rows8 + kTargetTile - 1) / kTargetTile);
+  const int64_t want = (1184 + tiles8 - 1) / tiles8;  // 148 SMs x 8 CTAs at 8 GPUs
+  const int64_t maxg = std::max<int64_t>(1, c->n_src_tiles / 4);
+  const int64_t g = std::max<int64_t>(1, std::min(want, maxg));
+  c->tiles_per_group = (int)((c->n_src_tiles + g - 1) / g);
+  c->n_groups = (c->n_src_tiles + c->tiles_per_group - 1) / c->tiles_per_group;
+}
+
+static int common_init(hobi_ctx* c, int device, double eps1, double eps2, double kappa) {
+  if (!(eps1 > 0.0)) return fail(HOBI_ERR_VALUE, "eps1 must be positive, got " + std::to_string(eps1));
+  if (!(eps2 > 0.0)) return fail(HOBI_ERR_VALUE, "eps2 must be positive, got " + std::to_string(eps2));
+  if (!(kappa >= 0.0))
+    return fail(HOBI_ERR_VALUE, "kappa must be nonnegative, got " + std::to_string(kappa));
+  c->device = device;
+  HOBI_CUDA(cudaSetDevice(device));
+  HOBI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  HOBI_CUDA(cudaEventCreate(&c->ev0));
+  HOBI_CUDA(cudaEventCreate(&c->ev1));
+  Physics& p = c->phys;
+  p.eps1 = eps1;
+  p.eps2 = eps2;
+  p.kappa = kappa;
+  p.er = eps2 / eps1;  // kernels.py:109
+  p.ier = 1.0 / p.er;
+  p.diag1 = 0.5 * (1.0 + p.er);
+  p.diag2 = 0.5 * (1.0 + 1.0 / p.er);
+  p.mode = kappa > 0.0 ? kScreened : kLaplace;
+  p.len_scale = p.mode == kScreened ? kappa : 1.0;
+  int rc;
+  if ((rc = upload_exp_table())) return rc;
+  return 0;
+}
+
+static int alloc_operands(hobi_ctx* c) {
+  c->nt_pad = ((c->nt + kTargetTile - 1) / kTargetTile) * kTargetTile;
+  c->ns_pad = std::max<int64_t>(kSrcTile, ((c->ns + kSrcTile - 1) / kSrcTile) * kSrcTile);
+  choose_groups(c);
+  if (c->tgt.alloc(6 * c->nt_pad) || c->src.alloc(c->ns_pad * kSrcStride) ||
+      c->part.alloc((size_t)c->n_groups * 2 * c->nt_pad) || c->u.alloc(std::max<int64_t>(1, 2 * c->nt)) ||
+      c->out.alloc(std::max<int64_t>(1, 2 * c->nt)))
+    return HOBI_ERR_CUDA;
+  c->lo = 0;
+  c->hi = c->nt;
+  int rc;
+  if (c->nt > 0 && (rc = prepare_targets(c))) return rc;
+  if ((rc = prepare_static_sources(c))) return rc;
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+// Scale check for the table-driven exp (valid for kappa*r < 1e12).
+static int check_extent(hobi_ctx* c, const double* v, int64_t n) {
+  if (c->phys.mode != kScreened) return 0;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], v[3 * i + k]);
+      hi[k] = std::max(hi[k], v[3 * i + k]);
+    }
+  double diag = 0.0;
+  for (int k = 0; k < 3; ++k) diag += (hi[k] - lo[k]) * (hi[k] - lo[k]);
+  if (c->phys.kappa * std::sqrt(diag) > 1e9)
+    return fail(HOBI_ERR_VALUE, "kappa * mesh extent exceeds the supported range (1e9)");
+  return 0;
+}
+
+}  // namespace hobi
+
+using namespace hobi;
+
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char* hobi_last_error(void) { return g_last_error.c_str(); }
+
+int hobi_abi_version(void) { return HOBI_ABI_VERSION; }
+
+int hobi_device_count(int* count) {
+  *count = 0;
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  return 0;
+}
+
+int hobi_create(int device, const double* vertices, const double* normals, int64_t nv,
+                const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
+                const double* reg_pts, const double* reg_wts, const double* reg_shape, int nq,
+                const double* duf_pts, const double* duf_wts, const double* duf_shape, int nd,
+                hobi_ctx** out) {
+  *out = nullptr;
+  if (nq < 1 || nq > 16) return fail(HOBI_ERR_VALUE, "regular rule must have 1..16 points");
+  if (nd < 1 || nd > 64) return fail(HOBI_ERR_VALUE, "Duffy rule must have 1..64 points");
+  if (nv < 1 || nf < 1) return fail(HOBI_ERR_VALUE, "mesh must have vertices and faces");
+  if (nv >= (1ll << 31) || 3 * nf >= (1ll << 31)) return fail(HOBI_ERR_VALUE, "mesh too large");
+  for (int64_t i = 0; i < 3 * nf; ++i)
+    if (faces[i] < 0 || faces[i] >= nv)
+      return fail(HOBI_ERR_VALUE, "face " + std::to_string(i / 3) + " references a vertex outside [0, " +
+                                      std::to_string(nv) + ")");
+  hobi_ctx* c = new hobi_ctx();
+  int rc;
+  auto bail = [&](int r) {
+    hobi_destroy(c);
+    return r;
+  };
+  if ((rc = common_init(c, device, eps1, eps2, kappa))) return bail(rc);
+  if ((rc = check_extent(c, vertices, nv))) return bail(rc);
+  c->scheme = kHobi;
+  c->nv = nv;
+  c->nf = nf;
+  c->nt = nv;
+  c->nq = nq;
+  c->nd = nd;
+  c->ns = nf * nq;
+  const int64_t np = 3 * nf;
+  // Pair tables (solver.py:229-243): slot 3f+k couples faces[f,k] with face f;
+  // a stable counting sort by vertex realises lexsort((pair_face, pair_vertex)).
+  std::vector<int> count(nv + 1, 0), pv(np), pf(np), pg(3 * np), slot_to_pair(np);
+  for (int64_t s = 0; s < np; ++s) count[faces[s] + 1]++;
+  for (int64_t v = 0; v < nv; ++v) count[v + 1] += count[v];
+  c->h_pair_starts.assign(count.begin(), count.end());
+  std::vector<int> fill(count.begin(), count.end() - 1);
+  for (int64_t s = 0; s < np; ++s) {
+    const int64_t f = s / 3, k = s % 3;
+    const int v = (int)faces[s];
+    const int p = fill[v]++;
+    slot_to_pair[s] = p;
+    pv[p] = v;
+    pf[p] = (int)f;
+    for (int q = 0; q < 3; ++q) pg[3 * p + q] = (int)faces[3 * f + (k + q) % 3];
+  }
+  std::vector<int> faces32(3 * nf);
+  for (int64_t i = 0; i < 3 * nf; ++i) faces32[i] = (int)faces[i];
+  std::vector<double> rbary(3 * nq), dbary(3 * nd);
+  for (int m = 0; m < nq; ++m) {  // _barycentric (solver.py:158-162)
+    rbary[3 * m] = 1.0 - reg_pts[2 * m] - reg_pts[2 * m + 1];
+    rbary[3 * m + 1] = reg_pts[2 * m];
+    rbary[3 * m + 2] = reg_pts[2 * m + 1];
+  }
+  for (int m = 0; m < nd; ++m) {
+    dbary[3 * m] = 1.0 - duf_pts[2 * m] - duf_pts[2 * m + 1];
+    dbary[3 * m + 1] = duf_pts[2 * m];
+    dbary[3 * m + 2] = duf_pts[2 * m + 1];
+  }
+  if (c->vert.alloc(3 * nv) || c->vnrm.alloc(3 * nv) || c->faces.alloc(3 * nf) ||
+      c->reg_pos.alloc(3 * nf * nq) || c->reg_nrm.alloc(3 * nf * nq) || c->reg_w.alloc(nf * nq) ||
+      c->duf_pos.alloc(3 * np * nd) || c->duf_nrm.alloc(3 * np * nd) || c->duf_w.alloc(np * nd) ||
+      c->pair_vertex.alloc(np) || c->pair_face.alloc(np) || c->pair_gverts.alloc(3 * np) ||
+      c->pair_starts.alloc(nv + 1) || c->reg_bary.alloc(3 * nq) || c->duf_bary.alloc(3 * nd) ||
+      c->corr.alloc(2 * np))
+    return bail(HOBI_ERR_CUDA);
+  auto up = [&](void* d, const void* h, size_t bytes) {
+    return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream);
+  };
+  cudaError_t e = cudaSuccess;
+  if (!e) e = up(c->vert.p, vertices, 3 * nv * sizeof(double));
+  if (!e) e = up(c->vnrm.p, normals, 3 * nv * sizeof(double));
+  if (!e) e = up(c->faces.p, faces32.data(), 3 * nf * sizeof(int));
+  if (!e) e = up(c->pair_vertex.p, pv.data(), np * sizeof(int));
+  if (!e) e = up(c->pair_face.p, pf.data(), np * sizeof(int));
+  if (!e) e = up(c->pair_gverts.p, pg.data(), 3 * np * sizeof(int));
+  if (!e) e = up(c->pair_starts.p, count.data(), (nv + 1) * sizeof(int));
+  if (!e) e = up(c->reg_bary.p, rbary.data(), 3 * nq * sizeof(double));
+  if (!e) e = up(c->duf_bary.p, dbary.data(), 3 * nd * sizeof(double));
+  if (e) return bail(cuda_fail(e, "cudaMemcpyAsync(upload)"));
+  if ((rc = upload_rule_tables(reg_shape, nq, duf_shape, nd, reg_wts, duf_wts))) return bail(rc);
+  int bad_slot = -1, bad_code = 0;
+  if ((rc = build_geometry(c, slot_to_pair.data(), &bad_slot, &bad_code))) return bail(rc);
+  if (bad_slot >= 0) {
+    static const char* msgs[] = {"", "arc endpoints coincide",
+                                 "endpoint normal is nearly parallel to the chord",
+                                 "endpoint normals are antiparallel"};
+    return bail(fail(HOBI_ERR_DEGENERATE_ARC,
+                     "face " + std::to_string(bad_slot / 3) + ": " + msgs[bad_code & 3]));
+  }
+  if ((rc = alloc_operands(c))) return bail(rc);
+  *out = c;
+  return 0;
+}
+
+int hobi_create_lobi(int device, const double* vertices, const double* normals, int64_t nv,
+                     const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
+                     hobi_ctx** out) {
+  (void)normals;
+  *out = nullptr;
+  if (nv < 1 || nf < 1) return fail(HOBI_ERR_VALUE, "mesh must have vertices and faces");
+  hobi_ctx* c = new hobi_ctx();
+  auto bail = [&](int r) {
+    hobi_destroy(c);
+    return r;
+  };
+  int rc;
+  if ((rc = common_init(c, device, eps1, eps2, kappa))) return bail(rc);
+  if ((rc = check_extent(c, vertices, nv))) return bail(rc);
+  c->scheme = kLobi;
+  c->nv = nv;
+  c->nf = nf;
+  c->nt = nf;
+  c->ns = nf;
+  c->nq = 1;
+  // flat centroids, unit normals, areas (solver.py:173-186)
+  std::vector<double> cen(3 * nf), nrm(3 * nf), area(nf);
+  for (int64_t f = 0; f < nf; ++f) {
+    const double* a = vertices + 3 * faces[3 * f];
+    const double* b = vertices + 3 * faces[3 * f + 1];
+    const double* d = vertices + 3 * faces[3 * f + 2];
+    double e1[3], e2[3];
+    for (int k = 0; k < 3; ++k) {
+      cen[3 * f + k] = ((a[k] + b[k]) + d[k]) / 3.0;
+      e1[k] = b[k] - a[k];
+      e2[k] = d[k] - a[k];
+    }
+    double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                    e1[0] * e2[1] - e1[1] * e2[0]};
+    volatile double s = cr[0] * cr[0];  // unfused left-to-right, like np.linalg.norm(axis=1)
+    s = s + cr[1] * cr[1];
+    s = s + cr[2] * cr[2];
+    double two = std::sqrt((double)s);
+    for (int k = 0; k < 3; ++k) nrm[3 * f + k] = cr[k] / two;
+    area[f] = 0.5 * two;
+  }
+  if (c->reg_pos.alloc(3 * nf) || c->reg_nrm.alloc(3 * nf) || c->lobi_area.alloc(nf))
+    return bail(HOBI_ERR_CUDA);
+  HOBI_CUDA(cudaMemcpy(c->reg_pos.p, cen.data(), 3 * nf * sizeof(double), cudaMemcpyHostToDevice));
+  HOBI_CUDA(cudaMemcpy(c->reg_nrm.p, nrm.data(), 3 * nf * sizeof(double), cudaMemcpyHostToDevice));
+  HOBI_CUDA(cudaMemcpy(c->lobi_area.p, area.data(), nf * sizeof(double), cudaMemcpyHostToDevice));
+  if ((rc = alloc_operands(c))) return bail(rc);
+  *out = c;
+  return 0;
+}
+
+int hobi_destroy(hobi_ctx* c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  if (c->comm.nccl && nccl::api().loaded) nccl::api().destroy(c->comm.nccl);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  cudaStream_t s = c->stream;
+  delete c;  // DevBufs free themselves
+  if (s) cudaStreamDestroy(s);
+  return 0;
+}
+
+int hobi_size(hobi_ctx* c, int64_t* n_colloc, int64_t* n_sources) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (n_colloc) *n_colloc = c->nt;
+  if (n_sources) *n_sources = c->ns;
+  return 0;
+}
+
+int hobi_matvec_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  return matvec_full_device(c, u_dev, out_dev);
+}
+
+int hobi_matvec(hobi_ctx* c, const double* u, double* out) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  const size_t bytes = 2 * c->nt * sizeof(double);
+  if (c->nt == 0) return 0;
+  HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, bytes, cudaMemcpyHostToDevice, c->stream));
+  int rc = matvec_full_device(c, c->u.p, c->out.p);
+  if (rc) return rc;
+  HOBI_CUDA(cudaMemcpyAsync(out, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int hobi_matvec_rows(hobi_ctx* c, const double* u, int64_t lo, int64_t hi, double* o1, double* o2) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (lo < 0 || hi > c->nt || lo > hi) return fail(HOBI_ERR_VALUE, "row range outside [0, n)");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  if (hi == lo) return 0;
+  HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, 2 * c->nt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int rc = matvec_rows_device(c, c->u.p, lo, hi, c->out.p, c->out.p + (hi - lo));
+  if (rc) return rc;
+  HOBI_CUDA(cudaMemcpyAsync(o1, c->out.p, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HOBI_CUDA(cudaMemcpyAsync(o2, c->out.p + (hi - lo), (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int hobi_rhs(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, double* b) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  int rc = rhs_device(c, qpos, q, nc, c->out.p);
+  if (rc) return rc;
+  HOBI_CUDA(cudaMemcpyAsync(b, c->out.p, 2 * c->nt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int hobi_energy(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, const double* phi,
+                const double* dphi, double* energy) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  HOBI_CUDA(cudaMemcpyAsync(c->u.p, phi, c->nt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  HOBI_CUDA(cudaMemcpyAsync(c->u.p + c->nt, dphi, c->nt * sizeof(double), cudaMemcpyHostToDevice,
+                            c->stream));
+  return energy_device(c, qpos, q, nc, c->u.p, energy);
+}
+
+namespace {
+struct CtxOperator : DeviceOperator {
+  hobi_ctx* c;
+  explicit CtxOperator(hobi_ctx* ctx) : c(ctx) {}
+  int apply(const double* in, double* out) override { return matvec_full_device(c, in, out); }
+};
+
+struct HostOperator : DeviceOperator {
+  hobi_apply_fn fn;
+  void* user;
+  int64_t n;
+  cudaStream_t stream;
+  std::vector<double> hin, hout;
+  HostOperator(hobi_apply_fn f, void* u, int64_t nn, cudaStream_t s)
+      : fn(f), user(u), n(nn), stream(s), hin(nn), hout(nn) {}
+  int apply(const double* in, double* out) override {
+    HOBI_CUDA(cudaMemcpyAsync(hin.data(), in, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    HOBI_CUDA(cudaStreamSynchronize(stream));
+    if (fn(user, hin.data(), hout.data(), n)) return fail(HOBI_ERR_VALUE, "operator callback failed");
+    HOBI_CUDA(cudaMemcpyAsync(out, hout.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
+    HOBI_CUDA(cudaStreamSynchronize(stream));
+    return 0;
+  }
+};
+}  // namespace
+
+int hobi_gmres(hobi_ctx* c, const double* b, double tol, int restart, int max_it, double* x,
+               int* iterations, double* residual, double* best, int* matvecs) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  CtxOperator op(c);
+  return gmres_device(c->device, c->stream, 2 * c->nt, &op, b, tol, restart, max_it, x, iterations,
+                      residual, best, matvecs, &c->launches);
+}
+
+int hobi_gmres_host_operator(int device, int64_t n, hobi_apply_fn apply, void* user, const double* b,
+                             double tol, int restart, int max_it, double* x, int* iterations,
+                             double* residual, double* best, int* matvecs) {
+  HOBI_CUDA(cudaSetDevice(device));
+  cudaStream_t s;
+  HOBI_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  int rc;
+  {
+    HostOperator op(apply, user, n, s);
+    rc = gmres_device(device, s, n, &op, b, tol, restart, max_it, x, iterations, residual, best,
+                      matvecs, nullptr);
+  }
+  cudaStreamDestroy(s);
+  return rc;
+}
+
+int hobi_export_caches(hobi_ctx* c, double* reg_pos, double* reg_nrm, double* reg_w, double* duf_pos,
+                       double* duf_nrm, double* duf_w, int64_t* pair_vertex, int64_t* pair_face,
+                       int64_t* pair_gverts, int64_t* pair_starts) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (c->scheme != kHobi) return fail(HOBI_ERR_VALUE, "caches exist only for scheme 'hobi'");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  const int64_t np = 3 * c->nf;
+  auto dn = [&](void* h, const void* d, size_t bytes) -> int {
+    if (!h) return 0;
+    HOBI_CUDA(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost));
+    return 0;
+  };
+  auto di = [&](int64_t* h, const int* d, int64_t n) -> int {
+    if (!h) return 0;
+    std::vector<int> t(n);
+    HOBI_CUDA(cudaMemcpy(t.data(), d, n * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) h[i] = t[i];
+    return 0;
+  };
+  int rc;
+  if ((rc = dn(reg_pos, c->reg_pos.p, 3 * c->nf * c->nq * sizeof(double)))) return rc;
+  if ((rc = dn(reg_nrm, c->reg_nrm.p, 3 * c->nf * c->nq * sizeof(double)))) return rc;
+  if ((rc = dn(reg_w, c->reg_w.p, c->nf * c->nq * sizeof(double)))) return rc;
+  if ((rc = dn(duf_pos, c->duf_pos.p, 3 * np * c->nd * sizeof(double)))) return rc;
+  if ((rc = dn(duf_nrm, c->duf_nrm.p, 3 * np * c->nd * sizeof(double)))) return rc;
+  if ((rc = dn(duf_w, c->duf_w.p, np * c->nd * sizeof(double)))) return rc;
+  if ((rc = di(pair_vertex, c->pair_vertex.p, np))) return rc;
+  if ((rc = di(pair_face, c->pair_face.p, np))) return rc;
+  if ((rc = di(pair_gverts, c->pair_gverts.p, 3 * np))) return rc;
+  if ((rc = di(pair_starts, c->pair_starts.p, c->nv + 1))) return rc;
+  return 0;
+}
+
+int hobi_kernel_values(int device, const double* d, const double* nx, const double* ny, int64_t n,
+                       double eps1, double eps2, double kappa, double* k) {
+  HOBI_CUDA(cudaSetDevice(device));
+  return kernel_values_device(d, nx, ny, n, eps1, eps2, kappa, k);
+}
+
+int hobi_comm_unique_id(unsigned char id[128]) {
+  auto& a = nccl::api();
+  if (!a.loaded) return fail(HOBI_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  nccl::UniqueId u;
+  int rc = nccl::check(a.get_unique_id(&u), "ncclGetUniqueId");
+  if (rc) return rc;
+  memcpy(id, u.internal, 128);
+  return 0;
+}
+
+int hobi_comm_init(hobi_ctx* c, const unsigned char id[128], int nranks, int rank) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(HOBI_ERR_VALUE, "bad rank/nranks");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  c->comm = Comm();
+  c->comm.nranks = nranks;
+  c->comm.rank = rank;
+  row_range(c->nt, nranks, rank, &c->lo, &c->hi);
+  if (nranks == 1) return 0;
+  auto& a = nccl::api();
+  if (!a.loaded) return fail(HOBI_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  nccl::UniqueId u;
+  memcpy(u.internal, id, 128);
+  int rc = nccl::check(a.init_rank(&c->comm.nccl, nranks, u, rank), "ncclCommInitRank");
+  if (rc) return rc;
+  return setup_gather(c, nranks);
+}
+
+int hobi_emulate_ranks(hobi_ctx* c, int nranks) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (nranks < 1) return fail(HOBI_ERR_VALUE, "nranks must be >= 1");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  c->comm = Comm();
+  c->comm.nranks = nranks;
+  c->comm.emulated = nranks > 1;
+  c->lo = 0;
+  c->hi = c->nt;
+  if (nranks == 1) return 0;
+  return setup_gather(c, nranks);
+}
+
+int hobi_timing_reset(hobi_ctx* c) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  c->sweep_ms = 0.0;
+  c->sweep_launches = 0;
+  c->launches = 0;
+  return 0;
+}
+
+int hobi_timing(hobi_ctx* c, double* sweep_ms, int64_t* sweep_launches, int64_t* all_launches) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (sweep_ms) *sweep_ms = c->sweep_ms;
+  if (sweep_launches) *sweep_launches = c->sweep_launches;
+  if (all_launches) *all_launches = c->launches;
+  return 0;
+}
+
+int hobi_pairs_per_matvec(hobi_ctx* c, double* pairs) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  *pairs = (double)c->nt * (double)c->ns;
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// FP64 roofline probe: 8 independent DFMA chains per thread.
+
+namespace {
+__global__ void dfma_probe_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-3, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+  double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 123.456) out[0] = s;
+}
+}  // namespace
+
+extern "C" int hobi_probe_fp64_tflops(int device, double ms, double* tflops) {
+  *tflops = 0.0;
+  HOBI_CUDA(cudaSetDevice(device));
+  int sms = 0;
+  HOBI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  DevBuf<double> d;
+  if (d.alloc(1)) return HOBI_ERR_CUDA;
+  const int blocks = sms * 8, threads = 256, iters = 2048;
+  cudaEvent_t e0, e1;
+  HOBI_CUDA(cudaEventCreate(&e0));
+  HOBI_CUDA(cudaEventCreate(&e1));
+  for (int w = 0; w < 3; ++w) dfma_probe_kernel<<<blocks, threads>>>(d.p, iters, 0.999999, 1e-7);
+  HOBI_CUDA(cudaDeviceSynchronize());
+  double total_ms = 0.0, flops = 0.0;
+  float best = 1e30f;
+  while (total_ms < ms) {
+    HOBI_CUDA(cudaEventRecord(e0));
+    dfma_probe_kernel<<<blocks, threads>>>(d.p, iters, 0.999999, 1e-7);
+    HOBI_CUDA(cudaEventRecord(e1));
+    HOBI_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    HOBI_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    best = std::min(best, t);
+    total_ms += t;
+    flops = 2.0 * 32.0 * iters * (double)blocks * threads;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *tflops = flops / (best * 1e-3) * 1e-12;
+  return 0;
+}

@@ -1,0 +1,103 @@
+// FP64 pair arithmetic of the all-pairs sweep, hand-scheduled
+// for the B200 FP64 pipe.  See DESIGN.md "kernel algebra" for the derivation:
+// coordinates are pre-scaled by kappa so r' = kappa*r, the physical constants
+// (1/4pi, kappa^n, er, 1/er) are folded into six per-source weights, expm1 and
+// exp share one table-driven range reduction, and 1/r comes from the MUFU
+// rsqrt seed plus one third-order Newton step.  50 FP64 instructions per pair
+// (vs ~95 for a literal libdevice transcription of kernels.py:112-130).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace hobi {
+
+// 1/sqrt(x): MUFU.RSQ64H seed (rel err 2^-20, measured) refined by
+// y (1 + e/2 + 3e^2/8), e = 1 - x y^2: error O(e^3) < 1e-17.
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double t = x * y;
+  double e = fma(-t, y, 1.0);
+  double c = fma(e, 0.375, 0.5);
+  double ye = y * e;
+  return fma(ye, c, y);
+}
+
+// exp(-x) - 1 for 0 <= x < 1e12, computed as S(1+p) - 1 with S = 2^(k/256)
+// from a 256-entry table (shared memory) and p = e^f - 1 on |f| <= ln2/512
+// (degree-4 Taylor, truncation < 4e-17).  S - 1 is exact for S in [1/2, 1]
+// (Sterbenz), so small arguments keep expm1's relative accuracy.
+__device__ __forceinline__ double expm1_neg(double x, const double* __restrict__ etab) {
+  const double kInv = 369.32993046757463;      // 256/ln2
+  const double kMagic = 6755399441055744.0;    // 1.5*2^52: rounds to integer in the low word
+  const double kStep = 2.7076061740622863e-3;  // ln2/256
+  double kf = fma(-x, kInv, kMagic);
+  int k = __double2loint(kf);
+  double kd = kf - kMagic;
+  double f = fma(kd, -kStep, -x);
+  double p = fma(f, 4.1666666666666664e-2, 1.6666666666666666e-1);
+  p = fma(p, f, 0.5);
+  p = fma(p, f, 1.0);
+  p = p * f;
+  double T = etab[k & 255];
+  int n = k >> 8;
+  double S = __hiloint2double(__double2hiint(T) + (n << 20), __double2loint(T));
+  S = (n < -1000) ? 0.0 : S;
+  return fma(S, p, S - 1.0);
+}
+
+// Screened pair (kappa > 0), scaled coordinates.  Source weights:
+//   W1 = -k wd/4pi, A = k^2 er wp/4pi, B = k^2 (er-1) wp/4pi,
+//   C = k^2 wd/(4pi er), D = -k^2 (1-1/er) wd/4pi, W4 = k^3 wp/4pi.
+// acc1 += K1 wd + K2 wp ; acc2 += K3 wd + K4 wp   (solver.py:333-334)
+template <bool FULL>
+__device__ __forceinline__ void pair_screened(double tx, double ty, double tz, double nx, double ny,
+                                              double nz, double sx, double sy, double sz, double mx,
+                                              double my, double mz, double W1, double A, double B,
+                                              double C, double D, double W4,
+                                              const double* __restrict__ etab, double& acc1,
+                                              double& acc2) {
+  double dx = tx - sx, dy = ty - sy, dz = tz - sz;
+  double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+  double dny = fma(dx, mx, fma(dy, my, dz * mz));
+  double ir = rsqrt_fast(r2);
+  double r = r2 * ir;  // kappa * |x - y|
+  double ir2 = ir * ir;
+  double ir3 = ir2 * ir;
+  double em1 = expm1_neg(r, etab);
+  double kre = fma(r, em1, r);  // kr e^{-kr}
+  double a = em1 + kre;         // (1+kr)e^{-kr} - 1      (kernels.py:119)
+  acc1 = fma(em1 * ir, W1, acc1);                 // K1 wd
+  acc1 = fma(dny * ir3, fma(a, A, B), acc1);      // K2 wp
+  if (FULL) {
+    double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
+    double nn = fma(nx, mx, fma(ny, my, nz * mz));
+    acc2 = fma(dnx * ir3, fma(a, C, D), acc2);    // K3 wd
+    // K4 wp: b = 3a + kr*kre (kernels.py:120), K4 ~ a nn - b Q with Q = dnx dny / r^2
+    double Q = (dnx * dny) * ir2;
+    double P = fma(Q, -3.0, nn);
+    double z = (r * kre) * Q;
+    acc2 = fma(ir3 * W4, fma(a, P, -z), acc2);
+  }
+}
+
+// Unscreened pair (kappa == 0): K1 = K4 = 0 exactly, as in the reference
+// (expm1(0) = 0 makes a = b = 0).  Weights B = (er-1) wp/4pi, D = -(1-1/er) wd/4pi.
+template <bool FULL>
+__device__ __forceinline__ void pair_laplace(double tx, double ty, double tz, double nx, double ny,
+                                             double nz, double sx, double sy, double sz, double mx,
+                                             double my, double mz, double B, double D,
+                                             double& acc1, double& acc2) {
+  double dx = tx - sx, dy = ty - sy, dz = tz - sz;
+  double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+  double dny = fma(dx, mx, fma(dy, my, dz * mz));
+  double ir = rsqrt_fast(r2);
+  double ir3 = (ir * ir) * ir;
+  acc1 = fma(dny * ir3, B, acc1);
+  if (FULL) {
+    double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
+    acc2 = fma(dnx * ir3, D, acc2);
+  }
+}
+
+}  // namespace hobi

@@ -1,0 +1,263 @@
+// Device-resident restarted GMRES: gmres_solve,
+// solver.py:484-560.  The Krylov basis, iterate and residual live in HBM; one
+// cooperative kernel per inner step performs the whole modified Gram-Schmidt
+// sweep (j+1 dots and axpys plus the normalisation) with grid-wide barriers,
+// deterministic fixed-partition reductions and no host round trip except the
+// (j+2)-entry Hessenberg column.  Givens rotations, the stopping tests and the
+// triangular solve stay on the host in the reference's exact scalar order.
+#include <cooperative_groups.h>
+
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "hobi_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace hobi {
+
+namespace {
+
+constexpr int kGT = 256;  // threads per block
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = kGT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Fixed chunk of [0, n) owned by this block.
+__device__ __forceinline__ void chunk(int64_t n, int64_t* lo, int64_t* hi) {
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  *lo = min(n, (int64_t)blockIdx.x * per);
+  *hi = min(n, *lo + per);
+}
+
+__device__ __forceinline__ double fixed_total(const double* __restrict__ part) {
+  double s = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) s += part[b];
+  return s;
+}
+
+// Arnoldi step j: w <- w - sum_i h_ij v_i (MGS), h_{j+1,j} = ||w||,
+// v_{j+1} = w / h_{j+1,j} when > 1e-300 (solver.py:538-543).
+__global__ void __launch_bounds__(kGT) mgs_kernel(double* __restrict__ V, int64_t ldv, int64_t n, int j,
+                                                  double* __restrict__ w, double* __restrict__ part,
+                                                  double* __restrict__ hcol) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[kGT];
+  int64_t lo, hi;
+  chunk(n, &lo, &hi);
+  for (int i = 0; i <= j; ++i) {
+    const double* vi = V + (int64_t)i * ldv;
+    double acc = 0.0;
+    for (int64_t k = lo + threadIdx.x; k < hi; k += kGT) acc = fma(vi[k], w[k], acc);
+    double* pb = part + (i & 1) * gridDim.x;
+    double bs = block_sum(acc, sh);
+    if (threadIdx.x == 0) pb[blockIdx.x] = bs;
+    grid.sync();
+    const double h = fixed_total(pb);
+    if (blockIdx.x == 0 && threadIdx.x == 0) hcol[i] = h;
+    for (int64_t k = lo + threadIdx.x; k < hi; k += kGT) w[k] = __dsub_rn(w[k], __dmul_rn(h, vi[k]));
+  }
+  double acc = 0.0;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += kGT) acc = fma(w[k], w[k], acc);
+  double* pb = part + ((j + 1) & 1) * gridDim.x;
+  double bs = block_sum(acc, sh);
+  if (threadIdx.x == 0) pb[blockIdx.x] = bs;
+  grid.sync();
+  const double nrm = sqrt(fixed_total(pb));
+  if (blockIdx.x == 0 && threadIdx.x == 0) hcol[j + 1] = nrm;
+  if (nrm > 1e-300) {
+    double* vn = V + (int64_t)(j + 1) * ldv;
+    for (int64_t k = lo + threadIdx.x; k < hi; k += kGT) vn[k] = w[k] / nrm;
+  }
+}
+
+// r = b - Ax and block partials of ||r||^2.
+__global__ void residual_kernel(const double* __restrict__ b, const double* __restrict__ ax, int64_t n,
+                                double* __restrict__ r, double* __restrict__ part) {
+  __shared__ double sh[kGT];
+  int64_t lo, hi;
+  chunk(n, &lo, &hi);
+  double acc = 0.0;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += kGT) {
+    double v = ax ? b[k] - ax[k] : b[k];
+    if (r) r[k] = v;
+    acc = fma(v, v, acc);
+  }
+  double bs = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = bs;
+}
+
+__global__ void norm_finish_kernel(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x || blockIdx.x) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[b];
+  out[0] = sqrt(s);
+}
+
+__global__ void scale_kernel(const double* __restrict__ r, int64_t n, double beta, double* __restrict__ v) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) v[k] = r[k] / beta;
+}
+
+// x += V[:j]^T y  (solver.py:560)
+__global__ void update_kernel(const double* __restrict__ V, int64_t ldv, int64_t n, int j,
+                              const double* __restrict__ y, double* __restrict__ x) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double s = 0.0;
+  for (int i = 0; i < j; ++i) s = fma(V[(int64_t)i * ldv + k], y[i], s);
+  x[k] = x[k] + s;
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+struct Workspace {
+  DevBuf<double> V, w, x, r, b, part, hcol, nrm, y;
+  int64_t ldv = 0;
+  int grid = 1;
+};
+
+}  // namespace
+
+int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op, const double* b_host,
+                 double tol, int restart, int max_it, double* x_host, int* iterations,
+                 double* residual, double* best_out, int* matvecs, int64_t* launch_counter) {
+  if (n % 2) return fail(HOBI_ERR_VALUE, "vector length must be even: (phi, dphi/dn) halves");
+  if (!(tol > 0.0 && tol < 1.0)) return fail(HOBI_ERR_VALUE, "tolerance must be in (0, 1)");
+  if (restart < 1) return fail(HOBI_ERR_VALUE, "restart must be >= 1");
+  if (max_it < 1) return fail(HOBI_ERR_VALUE, "max_iterations must be >= 1");
+  *iterations = 0;
+  *residual = 0.0;
+  *best_out = std::numeric_limits<double>::infinity();
+  *matvecs = 0;
+  int64_t launches = 0;
+  const int m = restart;
+  Workspace ws;
+  int sms = 0, occ = 0;
+  HOBI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  HOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mgs_kernel, kGT, 0));
+  ws.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(occ, 1),
+                                                         std::min<int64_t>(2 * sms, (n + 1023) / 1024)));
+  ws.ldv = ((n + 31) / 32) * 32;
+  if (ws.V.alloc((size_t)(m + 1) * ws.ldv) || ws.w.alloc(n) || ws.x.alloc(n) || ws.r.alloc(n) ||
+      ws.b.alloc(n) || ws.part.alloc(2 * ws.grid) || ws.hcol.alloc(m + 2) || ws.nrm.alloc(1) ||
+      ws.y.alloc(m))
+    return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemcpyAsync(ws.b.p, b_host, n * sizeof(double), cudaMemcpyHostToDevice, stream));
+
+  auto norm_of = [&](const double* ax, double* rout, double* val) -> int {
+    residual_kernel<<<ws.grid, kGT, 0, stream>>>(ws.b.p, ax, n, rout, ws.part.p);
+    norm_finish_kernel<<<1, 32, 0, stream>>>(ws.part.p, ws.grid, ws.nrm.p);
+    launches += 2;
+    HOBI_CUDA(cudaGetLastError());
+    HOBI_CUDA(cudaMemcpyAsync(val, ws.nrm.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    HOBI_CUDA(cudaStreamSynchronize(stream));
+    return 0;
+  };
+  int rc;
+  double norm_b = 0.0;
+  if ((rc = norm_of(nullptr, nullptr, &norm_b))) return rc;
+  if (norm_b == 0.0) {
+    std::fill(x_host, x_host + n, 0.0);
+    if (launch_counter) *launch_counter += launches;
+    return 0;
+  }
+  HOBI_CUDA(cudaMemsetAsync(ws.x.p, 0, n * sizeof(double), stream));
+  int total = 0;
+  double best = std::numeric_limits<double>::infinity();
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hcol(m + 2), y(m);
+  auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * m + j]; };
+  while (true) {
+    if ((rc = op->apply(ws.x.p, ws.w.p))) return rc;
+    ++*matvecs;
+    double rn = 0.0;
+    if ((rc = norm_of(ws.w.p, ws.r.p, &rn))) return rc;
+    const double rel = rn / norm_b;
+    best = std::min(best, rel);
+    if (rel <= tol) {
+      *iterations = total;
+      *residual = rel;
+      *best_out = best;
+      HOBI_CUDA(cudaMemcpyAsync(x_host, ws.x.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+      HOBI_CUDA(cudaStreamSynchronize(stream));
+      if (launch_counter) *launch_counter += launches;
+      return 0;
+    }
+    if (total >= max_it) {
+      *iterations = total;
+      *residual = rel;
+      *best_out = best;
+      if (launch_counter) *launch_counter += launches;
+      char msg[160];
+      snprintf(msg, sizeof(msg), "no convergence in %d iterations (best residual %.3e, tolerance %.3e)",
+               total, best, tol);
+      return fail(HOBI_ERR_NONCONVERGENCE, msg);
+    }
+    const double beta = rn;
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(cs.begin(), cs.end(), 0.0);
+    std::fill(sn.begin(), sn.end(), 0.0);
+    std::fill(g.begin(), g.end(), 0.0);
+    scale_kernel<<<nblk(n, 256), 256, 0, stream>>>(ws.r.p, n, beta, ws.V.p);
+    launches++;
+    g[0] = beta;
+    int j = 0;
+    while (j < m && total < max_it) {
+      if ((rc = op->apply(ws.V.p + (int64_t)j * ws.ldv, ws.w.p))) return rc;
+      ++*matvecs;
+      {
+        double* Vp = ws.V.p;
+        int64_t ldv = ws.ldv, nn = n;
+        int jj = j;
+        double *wp = ws.w.p, *pp = ws.part.p, *hp = ws.hcol.p;
+        void* args[] = {&Vp, &ldv, &nn, &jj, &wp, &pp, &hp};
+        HOBI_CUDA(cudaLaunchCooperativeKernel((const void*)mgs_kernel, dim3(ws.grid), dim3(kGT), args, 0,
+                                              stream));
+        launches++;
+      }
+      HOBI_CUDA(cudaMemcpyAsync(hcol.data(), ws.hcol.p, (j + 2) * sizeof(double),
+                                cudaMemcpyDeviceToHost, stream));
+      HOBI_CUDA(cudaStreamSynchronize(stream));
+      for (int i = 0; i <= j + 1; ++i) Hat(i, j) = hcol[i];
+      for (int i = 0; i < j; ++i) {  // apply previous rotations (solver.py:544-547)
+        double tmp = cs[i] * Hat(i, j) + sn[i] * Hat(i + 1, j);
+        Hat(i + 1, j) = -sn[i] * Hat(i, j) + cs[i] * Hat(i + 1, j);
+        Hat(i, j) = tmp;
+      }
+      double denom = std::hypot(Hat(j, j), Hat(j + 1, j));
+      cs[j] = Hat(j, j) / denom;
+      sn[j] = Hat(j + 1, j) / denom;
+      Hat(j, j) = denom;
+      Hat(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++total;
+      ++j;
+      if (std::fabs(g[j]) / norm_b <= tol) break;
+    }
+    // y = triu(H[:j,:j]) \ g[:j], column-oriented back substitution (solver.py:559)
+    for (int i = 0; i < j; ++i) y[i] = g[i];
+    for (int k = j - 1; k >= 0; --k) {
+      y[k] /= Hat(k, k);
+      for (int i = 0; i < k; ++i) y[i] -= y[k] * Hat(i, k);
+    }
+    if (j) {
+      HOBI_CUDA(cudaMemcpyAsync(ws.y.p, y.data(), j * sizeof(double), cudaMemcpyHostToDevice, stream));
+      update_kernel<<<nblk(n, 256), 256, 0, stream>>>(ws.V.p, ws.ldv, n, j, ws.y.p, ws.x.p);
+      launches++;
+      HOBI_CUDA(cudaGetLastError());
+    }
+  }
+}
+
+}  // namespace hobi

@@ -1,0 +1,154 @@
+// Internal declarations shared by the HOBI-PB CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hobi.h"
+
+namespace hobi {
+
+constexpr double kFourPi = 12.566370614359172;  // 4.0 * np.pi (kernels.py:27)
+constexpr double kKcal = 332.0716;               // kernels.py:33
+
+// Sweep tiling.
+constexpr int kSweepThreads = 128;  // threads per CTA
+constexpr int kSweepR = 2;          // targets held in registers per thread
+constexpr int kTargetTile = kSweepThreads * kSweepR;
+constexpr int kSrcTile = 64;        // sources per shared-memory stage
+constexpr int kSrcStride = 12;      // doubles per source record
+constexpr int kStages = 4;          // TMA bulk-copy pipeline depth
+constexpr int kExpTable = 256;      // 2^(j/256) table for the FP64 exp
+
+enum Scheme { kHobi = 0, kLobi = 1 };
+enum KernelMode { kLaplace = 0, kScreened = 1 };
+
+struct Error {
+  int status;
+  std::string msg;
+};
+
+void set_error(int status, const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define HOBI_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return hobi::cuda_fail(e_, #call); \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int alloc(size_t count) {
+    release();
+    n = count;
+    if (count == 0) return 0;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+// Constant physics, folded per scheme.
+struct Physics {
+  double eps1, eps2, kappa, er, ier;
+  double diag1, diag2;  // 0.5*(1+er), 0.5*(1+1/er)  (solver.py:365-366)
+  int mode;             // kLaplace when kappa == 0
+  double len_scale;     // kappa for kScreened (coordinates are pre-scaled), 1 otherwise
+};
+
+struct Comm {
+  void* nccl = nullptr;  // ncclComm_t
+  int nranks = 1;
+  int rank = 0;
+  bool emulated = false;
+};
+
+}  // namespace hobi
+
+struct hobi_ctx {
+  int device = 0;
+  int scheme = hobi::kHobi;
+  cudaStream_t stream = nullptr;
+  hobi::Physics phys{};
+  int64_t nv = 0, nf = 0;  // mesh sizes
+  int64_t nt = 0;          // collocation points (targets)
+  int64_t ns = 0;          // regular sources (nf*nq for hobi, nf for lobi)
+  int nq = 0, nd = 0;
+  int64_t ns_pad = 0, nt_pad = 0;
+  int n_src_tiles = 0, tiles_per_group = 0, n_groups = 0;
+  int64_t lo = 0, hi = 0;  // owned rows
+
+  // geometry (physical units)
+  hobi::DevBuf<double> vert, vnrm;           // (nv,3)
+  hobi::DevBuf<int> faces;                   // (nf,3)
+  hobi::DevBuf<double> reg_pos, reg_nrm, reg_w;  // (nf,nq,3),(nf,nq,3),(nf,nq)
+  hobi::DevBuf<double> duf_pos, duf_nrm, duf_w;  // pair order (3nf,nd,3)...
+  hobi::DevBuf<int> pair_vertex, pair_face, pair_gverts, pair_starts;
+  std::vector<int> h_pair_starts;
+  hobi::DevBuf<double> reg_bary, duf_bary;   // (nq,3), (nd,3)
+  hobi::DevBuf<double> lobi_area;            // (nf)
+  // sweep operands
+  hobi::DevBuf<double> tgt;                  // (6, nt_pad) scaled SoA
+  hobi::DevBuf<double> src;                  // (ns_pad, 12) scaled AoS records
+  hobi::DevBuf<double> part;                 // (n_groups, 2, nt_pad)
+  hobi::DevBuf<double> corr;                 // (3nf, 2) Duffy-minus-regular per pair
+  hobi::DevBuf<double> u, out;               // (2nt)
+  hobi::DevBuf<double> gather_send, gather_recv;  // (2*m), (nranks*2*m)
+  int64_t gather_m = 0;
+  hobi::Comm comm;
+
+  // instrumentation
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double sweep_ms = 0.0;
+  int64_t sweep_launches = 0;
+  int64_t launches = 0;
+  bool timing = true;
+};
+
+namespace hobi {
+
+// geometry (hobi_geometry.cu)
+int upload_rule_tables(const double* reg_shape, int nq, const double* duf_shape, int nd,
+                       const double* reg_wts, const double* duf_wts);
+int build_geometry(hobi_ctx* c, const int* pair_of_slot, int* first_bad_slot, int* bad_code);
+
+// sweep (hobi_sweep.cu)
+int upload_exp_table();
+int prepare_targets(hobi_ctx* c);
+int prepare_static_sources(hobi_ctx* c);
+int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi, double* o1,
+                       double* o2);
+int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev);
+int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc,
+                  const double* x_dev, double* energy);
+int rhs_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, double* b_dev);
+int kernel_values_device(const double* d, const double* nx, const double* ny, int64_t n,
+                         double eps1, double eps2, double kappa, double* k);
+
+// GMRES (hobi_gmres.cu)
+struct DeviceOperator {
+  virtual int apply(const double* in_dev, double* out_dev) = 0;
+  virtual ~DeviceOperator() {}
+};
+int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
+                 const double* b_host, double tol, int restart, int max_it, double* x_host,
+                 int* iterations, double* residual, double* best, int* matvecs,
+                 int64_t* launch_counter);
+
+// comm (hobi_api.cu)
+int comm_allgather(hobi_ctx* c);
+
+}  // namespace hobi

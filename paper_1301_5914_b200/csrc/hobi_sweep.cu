@@ -1,0 +1,465 @@
+// All-pairs regular sweep with its prologue (K-C: source
+// weights from u) and epilogue (K-D: group reduction + Duffy swap + diagonal),
+// plus the energy reduction (K-F) that reuses the sweep.
+//
+// Reference: _apply_range (solver.py:278-367) -> kernel_values_d
+// (kernels.py:99-130); solvation_energy (solver.py:581-614).
+//
+// Layout in HBM:
+//   tgt  : SoA (6, nt_pad)  x', y', z', nx, ny, nz   (x' = len_scale * x)
+//   src  : AoS (ns_pad, 12) x', y', z', nx, ny, nz, W1, A, B, C, D, W4
+//   part : (n_groups, 2, nt_pad) per-source-group partial sums
+// A CTA owns kTargetTile targets (kSweepR per thread, in registers) and one
+// fixed source group; source tiles of kSrcTile records stream through a
+// kStages-deep shared-memory ring filled by the TMA bulk-copy engine
+// (cp.async.bulk + mbarrier).  Source groups depend only on the problem, never
+// on the row split, so every row's sum is bitwise identical for any number of
+// GPUs (solver.py:12-17).
+#include <cmath>
+
+#include "hobi_fastmath.cuh"
+#include "hobi_internal.cuh"
+
+namespace hobi {
+
+__device__ double g_exp_table[kExpTable];
+
+int upload_exp_table() {
+  double t[kExpTable];
+  for (int j = 0; j < kExpTable; ++j) t[j] = (double)exp2l((long double)j / kExpTable);
+  HOBI_CUDA(cudaMemcpyToSymbol(g_exp_table, t, sizeof(t)));
+  return 0;
+}
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared, completion signalled on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr uint32_t kTileBytes = kSrcTile * kSrcStride * sizeof(double);
+constexpr size_t kSweepSmem =
+    (size_t)kStages * kTileBytes + kExpTable * sizeof(double) + kStages * sizeof(uint64_t);
+
+template <int MODE, bool FULL, bool SELF>
+__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
+    const double* __restrict__ tgt, int64_t ldt, int64_t t_begin, int64_t t_end,
+    const double* __restrict__ src, int n_src_tiles, int tiles_per_group, double* __restrict__ part,
+    int64_t ldp) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  double* etab = ring + kStages * kSrcTile * kSrcStride;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(etab + kExpTable);
+
+  const int g = blockIdx.y;
+  const int tile0 = g * tiles_per_group;
+  const int ntl = min(tiles_per_group, n_src_tiles - tile0);
+  const int64_t tb = t_begin + (int64_t)blockIdx.x * kTargetTile + threadIdx.x;
+
+  double tx[kSweepR], ty[kSweepR], tz[kSweepR], nx[kSweepR], ny[kSweepR], nz[kSweepR];
+  double a1[kSweepR], a2[kSweepR];
+#pragma unroll
+  for (int q = 0; q < kSweepR; ++q) {
+    int64_t t = min(tb + q * kSweepThreads, t_end - 1);  // padded threads recompute the last row
+    tx[q] = tgt[t];
+    ty[q] = tgt[ldt + t];
+    tz[q] = tgt[2 * ldt + t];
+    nx[q] = tgt[3 * ldt + t];
+    ny[q] = tgt[4 * ldt + t];
+    nz[q] = tgt[5 * ldt + t];
+    a1[q] = 0.0;
+    a2[q] = 0.0;
+  }
+  if (MODE == kScreened)
+    for (int i = threadIdx.x; i < kExpTable; i += kSweepThreads) etab[i] = g_exp_table[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double* gsrc = src + (int64_t)tile0 * kSrcTile * kSrcStride;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages - 1 && s < ntl; ++s) {
+      mbar_expect_tx(&bars[s], kTileBytes);
+      bulk_g2s(ring + s * kSrcTile * kSrcStride, gsrc + (int64_t)s * kSrcTile * kSrcStride,
+               kTileBytes, &bars[s]);
+    }
+  }
+  for (int it = 0; it < ntl; ++it) {
+    if (threadIdx.x == 0 && it + kStages - 1 < ntl) {
+      const int nxt = it + kStages - 1;
+      const int s = nxt % kStages;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[s], kTileBytes);
+      bulk_g2s(ring + s * kSrcTile * kSrcStride, gsrc + (int64_t)nxt * kSrcTile * kSrcStride,
+               kTileBytes, &bars[s]);
+    }
+    const int s = it % kStages;
+    mbar_wait(&bars[s], (uint32_t)((it / kStages) & 1));
+    const double2* rec = reinterpret_cast<const double2*>(ring + s * kSrcTile * kSrcStride);
+#pragma unroll 2
+    for (int j = 0; j < kSrcTile; ++j) {
+      const double2 p01 = rec[6 * j + 0], p2m0 = rec[6 * j + 1], m12 = rec[6 * j + 2];
+      double2 w01 = rec[6 * j + 3], w23 = rec[6 * j + 4], w45 = rec[6 * j + 5];
+#pragma unroll
+      for (int q = 0; q < kSweepR; ++q) {
+        double sx = p01.x, sy = p01.y, sz = p2m0.x;
+        if (SELF) {
+          // LOBI self pair: displacement forced to (1,0,0) and weights to 0, so
+          // it contributes exactly +0 (solver.py:303-310).
+          const bool self = ((int64_t)(tile0 + it) * kSrcTile + j) == tb + q * kSweepThreads;
+          if (self) {
+            sx = tx[q] - 1.0;
+            sy = ty[q];
+            sz = tz[q];
+            w01 = make_double2(0.0, 0.0);
+            w23 = w01;
+            w45 = w01;
+          }
+        }
+        if (MODE == kScreened)
+          pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz,
+                              p2m0.y, m12.x, m12.y, w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, etab,
+                              a1[q], a2[q]);
+        else
+          pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz,
+                             p2m0.y, m12.x, m12.y, w23.x, w45.x, a1[q], a2[q]);
+        if (SELF) {
+          w01 = rec[6 * j + 3];
+          w23 = rec[6 * j + 4];
+          w45 = rec[6 * j + 5];
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < kSweepR; ++q) {
+    int64_t t = tb + q * kSweepThreads;
+    if (t < t_end) {
+      part[(2 * (int64_t)g) * ldp + t] = a1[q];
+      if (FULL) part[(2 * (int64_t)g + 1) * ldp + t] = a2[q];
+    }
+  }
+}
+
+// Scaled static source geometry: record fields 0..5.
+__global__ void static_sources_kernel(const double* __restrict__ pos, const double* __restrict__ nrm,
+                                      int64_t ns, int64_t ns_pad, double scale,
+                                      double* __restrict__ src) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= ns_pad) return;
+  double* rec = src + s * kSrcStride;
+  if (s < ns) {
+    rec[0] = scale * pos[3 * s];
+    rec[1] = scale * pos[3 * s + 1];
+    rec[2] = scale * pos[3 * s + 2];
+    rec[3] = nrm[3 * s];
+    rec[4] = nrm[3 * s + 1];
+    rec[5] = nrm[3 * s + 2];
+  } else {  // padding: far away, unit normal, zero weights -> contributes +-0 exactly
+    rec[0] = 1e6 + (double)(s - ns);
+    rec[1] = 1e6;
+    rec[2] = 1e6;
+    rec[3] = 1.0;
+    rec[4] = 0.0;
+    rec[5] = 0.0;
+  }
+  for (int k = 6; k < 12; ++k) rec[k] = 0.0;
+}
+
+// Targets SoA, scaled.
+__global__ void targets_kernel(const double* __restrict__ pos, const double* __restrict__ nrm,
+                               int64_t nt, int64_t ldt, double scale, double* __restrict__ tgt) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ldt) return;
+  int64_t i = t < nt ? t : nt - 1;
+  tgt[t] = scale * pos[3 * i];
+  tgt[ldt + t] = scale * pos[3 * i + 1];
+  tgt[2 * ldt + t] = scale * pos[3 * i + 2];
+  tgt[3 * ldt + t] = nrm ? nrm[3 * i] : 1.0;
+  tgt[4 * ldt + t] = nrm ? nrm[3 * i + 1] : 0.0;
+  tgt[5 * ldt + t] = nrm ? nrm[3 * i + 2] : 0.0;
+}
+
+// K-C: interpolate u onto the regular points and fold the physics into the six
+// per-source weights.  phi_q = v0 b0 + v1 b1 + v2 b2 (solver.py:269-275),
+// wphi = reg_w * phi_q (solver.py:321-322).
+__global__ void source_weights_kernel(const double* __restrict__ u, int64_t nt,
+                                      const int* __restrict__ faces, const double* __restrict__ reg_w,
+                                      const double* __restrict__ bary, int nq, int64_t ns,
+                                      const double* __restrict__ area, double kA, double kB, double kC,
+                                      double kD, double kW1, double kW4, double* __restrict__ src) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= ns) return;
+  double wp, wd;
+  if (area) {  // LOBI: centroid collocation, weight = flat area (solver.py:297-298)
+    wp = area[s] * u[s];
+    wd = area[s] * u[nt + s];
+  } else {
+    int64_t f = s / nq;
+    int m = (int)(s - f * nq);
+    int i0 = faces[3 * f], i1 = faces[3 * f + 1], i2 = faces[3 * f + 2];
+    double b0 = bary[3 * m], b1 = bary[3 * m + 1], b2 = bary[3 * m + 2];
+    double ph = __dadd_rn(__dadd_rn(__dmul_rn(u[i0], b0), __dmul_rn(u[i1], b1)), __dmul_rn(u[i2], b2));
+    double dp = __dadd_rn(__dadd_rn(__dmul_rn(u[nt + i0], b0), __dmul_rn(u[nt + i1], b1)),
+                          __dmul_rn(u[nt + i2], b2));
+    double w = reg_w[s];
+    wp = w * ph;
+    wd = w * dp;
+  }
+  double* rec = src + s * kSrcStride;
+  rec[6] = kW1 * wd;
+  rec[7] = kA * wp;
+  rec[8] = kB * wp;
+  rec[9] = kC * wd;
+  rec[10] = kD * wd;
+  rec[11] = kW4 * wp;
+}
+
+// K-D: fixed-order group reduction + Duffy swap (solver.py:362-363) + diagonal
+// (solver.py:365-366).  Row v of [lo, hi) is written to o1[v-lo], o2[v-lo].
+__global__ void epilogue_kernel(const double* __restrict__ part, int64_t ldp, int n_groups,
+                                const double* __restrict__ corr, const int* __restrict__ pair_starts,
+                                const double* __restrict__ u, int64_t nt, int64_t lo, int64_t hi,
+                                double diag1, double diag2, double* __restrict__ o1,
+                                double* __restrict__ o2) {
+  int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= hi) return;
+  double acc1 = part[v], acc2 = part[ldp + v];
+  for (int g = 1; g < n_groups; ++g) {
+    acc1 += part[(2 * (int64_t)g) * ldp + v];
+    acc2 += part[(2 * (int64_t)g + 1) * ldp + v];
+  }
+  if (corr) {
+    double c1 = 0.0, c2 = 0.0;
+    for (int p = pair_starts[v]; p < pair_starts[v + 1]; ++p) {
+      c1 += corr[2 * (int64_t)p];
+      c2 += corr[2 * (int64_t)p + 1];
+    }
+    acc1 += c1;
+    acc2 += c2;
+  }
+  o1[v - lo] = __dsub_rn(__dmul_rn(diag1, u[v]), acc1);
+  o2[v - lo] = __dsub_rn(__dmul_rn(diag2, u[nt + v]), acc2);
+}
+
+// Gathered rank-major rows [r][2][m] -> out[0:nt] ++ out[nt:2nt].
+__global__ void permute_kernel(const double* __restrict__ recv, int64_t m, int64_t nt, int nranks,
+                               double* __restrict__ out) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nt) return;
+  int64_t base = nt / nranks, extra = nt % nranks;
+  int64_t cut = extra * (base + 1);
+  int64_t r = v < cut ? v / (base + 1) : extra + (v - cut) / (base ? base : 1);
+  int64_t lo = r < extra ? r * (base + 1) : cut + (r - extra) * base;
+  out[v] = recv[(r * 2) * m + (v - lo)];
+  out[nt + v] = recv[(r * 2 + 1) * m + (v - lo)];
+}
+
+__global__ void energy_reduce_kernel(const double* __restrict__ part, int64_t ldp, int n_groups,
+                                     const double* __restrict__ q, int64_t nc, double* __restrict__ out) {
+  // one thread, fixed order: total += q_k * sum_k (solver.py:608-614)
+  if (blockIdx.x || threadIdx.x) return;
+  double total = 0.0;
+  for (int64_t k = 0; k < nc; ++k) {
+    double s = part[k];
+    for (int g = 1; g < n_groups; ++g) s += part[(2 * (int64_t)g) * ldp + k];
+    total += q[k] * s;
+  }
+  out[0] = 0.5 * kFourPi * kKcal * total;
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_t t1, bool full,
+                 double* part, int64_t ldp, int n_groups, int tiles_per_group) {
+  if (t1 <= t0) return 0;
+  dim3 grid(nblk(t1 - t0, kTargetTile), n_groups);
+  const bool self = c->scheme == kLobi && full;
+  void (*fn)(const double*, int64_t, int64_t, int64_t, const double*, int, int, double*, int64_t);
+  if (c->phys.mode == kScreened)
+    fn = self ? sweep_kernel<kScreened, true, true>
+              : (full ? sweep_kernel<kScreened, true, false> : sweep_kernel<kScreened, false, false>);
+  else
+    fn = self ? sweep_kernel<kLaplace, true, true>
+              : (full ? sweep_kernel<kLaplace, true, false> : sweep_kernel<kLaplace, false, false>);
+  static bool attr_done[2][2][2] = {};
+  if (!attr_done[c->phys.mode][full][self]) {
+    HOBI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
+    attr_done[c->phys.mode][full][self] = true;
+  }
+  if (c->timing) HOBI_CUDA(cudaEventRecord(c->ev0, c->stream));
+  fn<<<grid, kSweepThreads, kSweepSmem, c->stream>>>(tgt, ldt, t0, t1, c->src.p, c->n_src_tiles,
+                                                     tiles_per_group, part, ldp);
+  HOBI_CUDA(cudaGetLastError());
+  c->launches++;
+  if (c->timing) {
+    HOBI_CUDA(cudaEventRecord(c->ev1, c->stream));
+    HOBI_CUDA(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    HOBI_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->sweep_ms += ms;
+    c->sweep_launches++;
+  }
+  return 0;
+}
+
+// Physics folded into the per-source weights (see hobi_fastmath.cuh).
+void weight_constants(const Physics& p, double* kA, double* kB, double* kC, double* kD, double* kW1,
+                      double* kW4) {
+  const double k = p.mode == kScreened ? p.kappa : 1.0;
+  const double k2 = k * k / kFourPi;
+  *kW1 = p.mode == kScreened ? -k / kFourPi : 0.0;
+  *kA = p.mode == kScreened ? k2 * p.er : 0.0;
+  *kB = k2 * (p.er - 1.0);
+  *kC = p.mode == kScreened ? k2 / p.er : 0.0;
+  *kD = -k2 * (1.0 - 1.0 / p.er);
+  *kW4 = p.mode == kScreened ? k * k2 : 0.0;
+}
+
+}  // namespace
+
+int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1);  // hobi_literal.cu
+
+int prepare_targets(hobi_ctx* c) {
+  const double* pos = c->scheme == kHobi ? c->vert.p : c->reg_pos.p;  // lobi: centroids
+  const double* nrm = c->scheme == kHobi ? c->vnrm.p : c->reg_nrm.p;
+  targets_kernel<<<nblk(c->nt_pad, 256), 256, 0, c->stream>>>(pos, nrm, c->nt, c->nt_pad,
+                                                              c->phys.len_scale, c->tgt.p);
+  c->launches++;
+  HOBI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int prepare_static_sources(hobi_ctx* c) {
+  static_sources_kernel<<<nblk(c->ns_pad, 256), 256, 0, c->stream>>>(
+      c->reg_pos.p, c->reg_nrm.p, c->ns, c->ns_pad, c->phys.len_scale, c->src.p);
+  c->launches++;
+  HOBI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+static int update_weights(hobi_ctx* c, const double* u_dev) {
+  double kA, kB, kC, kD, kW1, kW4;
+  weight_constants(c->phys, &kA, &kB, &kC, &kD, &kW1, &kW4);
+  source_weights_kernel<<<nblk(c->ns, 256), 256, 0, c->stream>>>(
+      u_dev, c->nt, c->faces.p, c->reg_w.p, c->reg_bary.p, c->nq, c->ns,
+      c->scheme == kLobi ? c->lobi_area.p : nullptr, kA, kB, kC, kD, kW1, kW4, c->src.p);
+  c->launches++;
+  HOBI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi, double* o1,
+                       double* o2) {
+  if (hi <= lo) return 0;
+  int rc;
+  if ((rc = update_weights(c, u_dev))) return rc;
+  if ((rc = launch_sweep(c, c->tgt.p, c->nt_pad, lo, hi, true, c->part.p, c->nt_pad, c->n_groups,
+                         c->tiles_per_group)))
+    return rc;
+  const double* corr = nullptr;
+  const int* starts = nullptr;
+  if (c->scheme == kHobi) {
+    if ((rc = launch_singular(c, u_dev, c->h_pair_starts[lo], c->h_pair_starts[hi]))) return rc;
+    corr = c->corr.p;
+    starts = c->pair_starts.p;
+  }
+  epilogue_kernel<<<nblk(hi - lo, 256), 256, 0, c->stream>>>(
+      c->part.p, c->nt_pad, c->n_groups, corr, starts, u_dev, c->nt, lo, hi, c->phys.diag1,
+      c->phys.diag2, o1, o2);
+  c->launches++;
+  HOBI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
+  int rc;
+  if (c->comm.nranks == 1) return matvec_rows_device(c, u_dev, 0, c->nt, out_dev, out_dev + c->nt);
+  const int64_t m = c->gather_m;
+  if (c->comm.emulated) {  // every rank's rows, computed here, in the gather layout
+    for (int r = 0; r < c->comm.nranks; ++r) {
+      int64_t base = c->nt / c->comm.nranks, extra = c->nt % c->comm.nranks;
+      int64_t lo = r * base + (r < extra ? r : extra);
+      int64_t hi = lo + base + (r < extra ? 1 : 0);
+      double* slot = c->gather_recv.p + (int64_t)r * 2 * m;
+      if ((rc = matvec_rows_device(c, u_dev, lo, hi, slot, slot + m))) return rc;
+    }
+  } else {
+    if ((rc = matvec_rows_device(c, u_dev, c->lo, c->hi, c->gather_send.p, c->gather_send.p + m)))
+      return rc;
+    if ((rc = comm_allgather(c))) return rc;
+  }
+  permute_kernel<<<nblk(c->nt, 256), 256, 0, c->stream>>>(c->gather_recv.p, m, c->nt,
+                                                           c->comm.nranks, out_dev);
+  c->launches++;
+  HOBI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, const double* x_dev,
+                  double* energy) {
+  *energy = 0.0;
+  if (nc == 0) return 0;
+  // charges act as targets of a K1/K2-only sweep over the regular points
+  // (solver.py:609-613); their "normal" is unused.
+  const int64_t ldc = ((nc + kTargetTile - 1) / kTargetTile) * kTargetTile;
+  DevBuf<double> dq, dqpos, tq, part, e;
+  if (dq.alloc(nc) || dqpos.alloc(3 * nc) || tq.alloc(6 * ldc) || e.alloc(1)) return HOBI_ERR_CUDA;
+  int tiles = c->n_src_tiles;
+  int tiles_per_group = std::max(4, (int)((tiles + 15) / 16));
+  int groups = (tiles + tiles_per_group - 1) / tiles_per_group;
+  if (part.alloc((size_t)groups * 2 * ldc)) return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemcpyAsync(dq.p, q, nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  HOBI_CUDA(cudaMemcpyAsync(dqpos.p, qpos, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  targets_kernel<<<nblk(ldc, 256), 256, 0, c->stream>>>(dqpos.p, nullptr, nc, ldc,
+                                                        c->phys.len_scale, tq.p);
+  c->launches++;
+  int rc;
+  if ((rc = update_weights(c, x_dev))) return rc;
+  bool timing = c->timing;
+  c->timing = false;
+  rc = launch_sweep(c, tq.p, ldc, 0, nc, false, part.p, ldc, groups, tiles_per_group);
+  c->timing = timing;
+  if (rc) return rc;
+  energy_reduce_kernel<<<1, 32, 0, c->stream>>>(part.p, ldc, groups, dq.p, nc, e.p);
+  c->launches++;
+  HOBI_CUDA(cudaGetLastError());
+  HOBI_CUDA(cudaMemcpyAsync(energy, e.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+}  // namespace hobi

@@ -1,0 +1,191 @@
+"""Surface meshes and point charges: the input contract of the hot path.
+
+Mirrors the reference's immutable input types and their validation
+(``pbbem/mesh.py:24-110``, ``validate`` at ``:50-89``) plus the icosahedral
+sphere generator (``:230-300``) used to build every benchmark surface.  File
+ingest (MSMS) is a later row of SURVEY.md section 8(f) and lives here too.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+class MeshFormatError(ValueError):
+    """A mesh or charge file could not be parsed (pbbem/mesh.py:16-17)."""
+
+
+class MeshValidationError(ValueError):
+    """A mesh violates a structural invariant (pbbem/mesh.py:20-21)."""
+
+
+def _frozen(a, dtype):
+    a = np.array(a, dtype=dtype)
+    a.setflags(write=False)
+    return a
+
+
+@dataclass(frozen=True)
+class FlatMesh:
+    """Closed triangulated surface with outward unit vertex normals (pbbem/mesh.py:24-75)."""
+
+    vertices: np.ndarray  # (n_v, 3) Angstrom
+    normals: np.ndarray  # (n_v, 3) unit
+    faces: np.ndarray  # (n_f, 3) int64, 0-based, outward winding
+
+    def __post_init__(self):
+        object.__setattr__(self, "vertices", _frozen(self.vertices, float).reshape(-1, 3))
+        object.__setattr__(self, "normals", _frozen(self.normals, float).reshape(-1, 3))
+        object.__setattr__(self, "faces", _frozen(self.faces, np.int64).reshape(-1, 3))
+
+    @property
+    def n_vertices(self) -> int:
+        return self.vertices.shape[0]
+
+    @property
+    def n_faces(self) -> int:
+        return self.faces.shape[0]
+
+    def validate(self) -> None:
+        """Unit normals, index range, orientation, closedness -- in the reference's order."""
+        n = self.normals
+        lengths = np.sqrt(n[:, 0] ** 2 + n[:, 1] ** 2 + n[:, 2] ** 2)
+        bad = np.flatnonzero(np.abs(lengths - 1.0) > 1e-12)
+        if bad.size:
+            raise MeshValidationError(
+                f"normal {bad[0]} has length {lengths[bad[0]]!r}, expected 1")
+        f = self.faces
+        nv = self.n_vertices
+        if f.size:
+            out = ((f < 0) | (f >= nv)).any(axis=1)
+            if out.any():
+                raise MeshValidationError(
+                    f"face {np.flatnonzero(out)[0]} references a vertex outside [0, {nv})")
+        x = self.vertices[f]
+        geo = np.cross(x[:, 1] - x[:, 0], x[:, 2] - x[:, 0])
+        mean_n = self.normals[f].mean(axis=1)
+        flipped = np.flatnonzero(np.einsum("ij,ij->i", geo, mean_n) <= 0.0)
+        if flipped.size:
+            raise MeshValidationError(
+                f"face {flipped[0]} is oriented against its vertex normals")
+        _check_closed(f)
+
+
+def _check_closed(faces: np.ndarray) -> None:
+    """Every undirected edge shared by exactly two faces (pbbem/mesh.py:78-89)."""
+    if faces.size == 0:
+        return
+    e = np.sort(np.concatenate([faces[:, [0, 1]], faces[:, [1, 2]], faces[:, [2, 0]]]), axis=1)
+    key = e[:, 0] * (int(e.max()) + 1) + e[:, 1]
+    uniq, counts = np.unique(key, return_counts=True)
+    bad = np.flatnonzero(counts != 2)
+    if bad.size:
+        k = int(uniq[bad[0]])
+        m = int(e.max()) + 1
+        raise MeshValidationError(
+            f"mesh is not closed: edge ({k // m}, {k % m}) belongs to {counts[bad[0]]} "
+            f"face(s), expected 2")
+
+
+@dataclass(frozen=True)
+class ChargeSystem:
+    """Point charges in Angstrom / elementary charges (pbbem/mesh.py:92-110)."""
+
+    positions: np.ndarray
+    charges: np.ndarray
+
+    def __post_init__(self):
+        p = _frozen(self.positions, float).reshape(-1, 3)
+        q = _frozen(self.charges, float).reshape(-1)
+        if p.shape[0] != q.shape[0]:
+            raise ValueError(f"{p.shape[0]} positions but {q.shape[0]} charges")
+        object.__setattr__(self, "positions", p)
+        object.__setattr__(self, "charges", q)
+
+    def __len__(self) -> int:
+        return self.charges.size
+
+
+# ----------------------------------------------------------------------------
+# icosahedral spheres (pbbem/mesh.py:230-300), vectorised subdivision
+
+
+def _base_icosahedron():
+    t = (1.0 + 5.0 ** 0.5) / 2.0
+    v = np.array([(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0),
+                  (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+                  (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)], dtype=float)
+    v /= np.linalg.norm(v[0])
+    f = np.array([(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11),
+                  (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6), (7, 1, 8),
+                  (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9),
+                  (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)], dtype=np.int64)
+    return v, f
+
+
+def _fma(a, b, c):
+    """Error-free-transform emulation of fused a*b+c (Dekker product + two-sum)."""
+    p = a * b
+    t = 134217729.0 * a
+    ah = t - (t - a)
+    t = 134217729.0 * b
+    bh = t - (t - b)
+    ep = ((ah * bh - p) + ah * (b - bh) + (a - ah) * bh) + (a - ah) * (b - bh)
+    s = p + c
+    bb = s - p
+    es = (p - (s - bb)) + (c - bb)
+    return s + (ep + es)
+
+
+def _blas_norm(m):
+    """Row norms with the same rounding as np.linalg.norm on one 3-vector
+    (OpenBLAS ddot: fma(z, z, fma(y, y, x*x))), so generated spheres match the
+    reference's vertex coordinates bit for bit."""
+    return np.sqrt(_fma(m[:, 2], m[:, 2], _fma(m[:, 1], m[:, 1], m[:, 0] * m[:, 0])))
+
+
+def _split(v, f):
+    """One 4-to-1 split.  New midpoint vertices are numbered in order of first
+    encounter over (face, edge ab/bc/ca), which reproduces the reference's
+    dictionary-insertion numbering (pbbem/mesh.py:281-300)."""
+    nf = f.shape[0]
+    a, b, c = f[:, 0], f[:, 1], f[:, 2]
+    ends = np.stack([np.stack([a, b], 1), np.stack([b, c], 1), np.stack([c, a], 1)], 1).reshape(-1, 2)
+    lo = ends.min(axis=1)
+    hi = ends.max(axis=1)
+    key = lo * v.shape[0] + hi
+    uniq, first, inv = np.unique(key, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")  # unique edges by first appearance
+    rank = np.empty_like(order)
+    rank[order] = np.arange(order.size)
+    mid_id = v.shape[0] + rank[inv].reshape(nf, 3)
+    e0 = ends[first[order]]
+    m = v[e0[:, 0]] + v[e0[:, 1]]
+    m = m / _blas_norm(m)[:, None]
+    ab, bc, ca = mid_id[:, 0], mid_id[:, 1], mid_id[:, 2]
+    nfaces = np.stack([np.stack([a, ab, ca], 1), np.stack([b, bc, ab], 1),
+                       np.stack([c, ca, bc], 1), np.stack([ab, bc, ca], 1)], 1).reshape(-1, 3)
+    return np.concatenate([v, m]), nfaces
+
+
+def unit_icosphere(level: int):
+    """Unit-sphere vertices and faces of the level-`level` subdivided icosahedron."""
+    if not 0 <= level <= 8:
+        raise ValueError(f"refinement level must be in [0, 8], got {level}")
+    v, f = _base_icosahedron()
+    for _ in range(level):
+        v, f = _split(v, f)
+    return v, f
+
+
+def icosahedral_sphere(level: int, radius: float = 1.0, center=(0.0, 0.0, 0.0)) -> FlatMesh:
+    """Subdivided icosahedron on a sphere with exact radial normals (pbbem/mesh.py:258-278)."""
+    if not 0 <= level <= 7:
+        raise ValueError(f"refinement level must be in [0, 7], got {level}")
+    if radius <= 0.0:
+        raise ValueError(f"radius must be positive, got {radius}")
+    v, f = unit_icosphere(level)
+    c = np.asarray(center, dtype=float)
+    return FlatMesh(vertices=c + radius * v, normals=v.copy(), faces=f)

@@ -1,0 +1,464 @@
+"""Host-side mirror of the reference solver API over the B200 C-ABI library.
+
+Same names, arguments, return types and error behaviour as
+``pbbem/solver.py`` (cited per function), but every array operation on the
+hot path -- geometry precompute, matvec, right-hand side, GMRES, energy --
+runs in hand-written sm_100a kernels behind ``libhobi.so``.  There is no CPU
+fallback: without the library or a CUDA device the calls raise.
+
+Parallelism: ``SolverConfig.workers`` keeps its meaning of "number of row
+partitions".  Under ``torch.distributed`` with world size > 1 (one process
+per GPU, e.g. torchrun) the partitions are the ranks and every matvec ends in
+one NCCL allgather over NVLink; in a single process a workers > 1 operator
+emulates the same split on one GPU.  Either way rows are bitwise identical to
+the unsplit operator (solver.py:12-17).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .mesh import ChargeSystem, FlatMesh
+from .physics import FOUR_PI, KCAL_MOL_PER_E2_ANG, PhysicalParams, SingularityError
+from .quadrature import TriangleRule, barycentric, duffy_rule, gauss_radau_rule, shape_tables
+
+SCHEMES = ("hobi", "lobi")
+
+
+class DegenerateArcError(ValueError):
+    """An edge arc could not be fitted (geometry.py:24-25)."""
+
+
+class GmresNonConvergence(RuntimeError):
+    """GMRES hit its iteration budget; carries the best residual (solver.py:50-55)."""
+
+    def __init__(self, message: str, best_residual: float):
+        super().__init__(message)
+        self.best_residual = best_residual
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """Solver knobs (solver.py:58-87); ``workers`` = row partitions (GPU ranks)."""
+
+    scheme: str = "hobi"
+    tolerance: float = 1e-6
+    restart: int = 100
+    max_iterations: int = 1000
+    workers: int | None = None
+    regular_rule: TriangleRule = field(default_factory=gauss_radau_rule)
+    duffy_points: int = 4
+
+    def __post_init__(self):
+        if self.scheme not in SCHEMES:
+            raise ValueError(f"scheme must be one of {SCHEMES}, got {self.scheme!r}")
+        if not 0.0 < self.tolerance < 1.0:
+            raise ValueError(f"tolerance must be in (0, 1), got {self.tolerance}")
+        if self.restart < 1:
+            raise ValueError(f"restart must be >= 1, got {self.restart}")
+        if self.max_iterations < 1:
+            raise ValueError(f"max_iterations must be >= 1, got {self.max_iterations}")
+        if self.workers is not None and self.workers < 1:
+            raise ValueError(f"workers must be >= 1, got {self.workers}")
+
+    def worker_count(self) -> int:
+        if self.workers is not None:
+            return self.workers
+        return _world()[1]
+
+
+@dataclass(frozen=True)
+class SurfaceSolution:
+    """Solved surface traces plus diagnostics (solver.py:90-102)."""
+
+    phi: np.ndarray
+    dphi_dn: np.ndarray
+    scheme: str
+    iterations: int
+    residual: float
+
+    @property
+    def vector(self) -> np.ndarray:
+        return np.concatenate([self.phi, self.dphi_dn])
+
+
+def _world():
+    """(rank, world_size, local_rank) of an initialised torch.distributed job."""
+    try:
+        import torch.distributed as dist
+    except Exception:  # noqa: BLE001
+        return 0, 1, 0
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, 1, 0
+    return dist.get_rank(), dist.get_world_size(), int(os.environ.get("LOCAL_RANK", dist.get_rank()))
+
+
+def _device_index() -> int:
+    if "HOBI_DEVICE" in os.environ:
+        return int(os.environ["HOBI_DEVICE"])
+    return _world()[2]
+
+
+class _Handle:
+    """Owns one native context (device caches live as long as this object)."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        if self.ptr:
+            try:
+                N.load().hobi_destroy(self.ptr)
+            except Exception:  # noqa: BLE001
+                pass
+            self.ptr = None
+
+
+def _raise(status: int):
+    if status == N.HOBI_OK:
+        return
+    msg = N.last_error()
+    if status == N.HOBI_ERR_DEGENERATE_ARC:
+        raise DegenerateArcError(msg)
+    if status == N.HOBI_ERR_SINGULARITY:
+        raise SingularityError(msg)
+    if status == N.HOBI_ERR_VALUE:
+        raise ValueError(msg)
+    raise N.NativeError(status, msg)
+
+
+class DiscretizedProblem:
+    """Device-resident discretisation (solver.py:105-155).
+
+    The reference's cache arrays are exposed as read-only properties copied
+    back from HBM on first access (the device copies are what the kernels
+    read).  ``n_collocation``, ``n_unknowns`` and ``singular_faces`` behave as
+    in the reference.
+    """
+
+    _CACHE = ("reg_pos", "reg_nrm", "reg_w", "duf_pos", "duf_nrm", "duf_w", "pair_vertex",
+              "pair_face", "pair_gverts", "pair_starts")
+
+    def __init__(self, mesh, params, charges, scheme, handle, rule, duffy, rank_info):
+        self.mesh = mesh
+        self.params = params
+        self.charges = charges
+        self.scheme = scheme
+        self._h = handle
+        self._rule = rule
+        self._duffy = duffy
+        self._cache = {}
+        self.rank, self.world = rank_info
+        if scheme == "hobi":
+            self.colloc_pos = mesh.vertices
+            self.colloc_nrm = mesh.normals
+            self.reg_bary = barycentric(rule.points)
+            self.duf_bary = barycentric(duffy.points)
+        else:
+            x = mesh.vertices[mesh.faces]
+            cr = np.cross(x[:, 1] - x[:, 0], x[:, 2] - x[:, 0])
+            two = np.linalg.norm(cr, axis=1)
+            self.colloc_pos = x.mean(axis=1)
+            self.colloc_nrm = cr / two[:, None]
+            self.area = 0.5 * two
+            self.reg_bary = self.duf_bary = None
+
+    @property
+    def handle(self):
+        return self._h.ptr
+
+    @property
+    def n_collocation(self) -> int:
+        return self.colloc_pos.shape[0]
+
+    @property
+    def n_unknowns(self) -> int:
+        return 2 * self.n_collocation
+
+    def _export(self):
+        if self._cache or self.scheme != "hobi":
+            return
+        nf, nq, nd = self.mesh.n_faces, len(self._rule), len(self._duffy)
+        out = {
+            "reg_pos": np.empty((nf, nq, 3)), "reg_nrm": np.empty((nf, nq, 3)), "reg_w": np.empty((nf, nq)),
+            "duf_pos": np.empty((3 * nf, nd, 3)), "duf_nrm": np.empty((3 * nf, nd, 3)),
+            "duf_w": np.empty((3 * nf, nd)), "pair_vertex": np.empty(3 * nf, np.int64),
+            "pair_face": np.empty(3 * nf, np.int64), "pair_gverts": np.empty((3 * nf, 3), np.int64),
+            "pair_starts": np.empty(self.mesh.n_vertices + 1, np.int64),
+        }
+        _raise(N.load().hobi_export_caches(
+            self.handle, *(N.dptr(out[k]) for k in self._CACHE[:6]),
+            *(N.iptr(out[k]) for k in self._CACHE[6:])))
+        for a in out.values():
+            a.setflags(write=False)
+        self._cache = out
+
+    def __getattr__(self, name):
+        if name in DiscretizedProblem._CACHE:
+            if self.scheme != "hobi":
+                return None
+            self._export()
+            return self._cache[name]
+        raise AttributeError(name)
+
+    def singular_faces(self, vertex: int) -> np.ndarray:
+        """Faces treated singularly for this vertex, face-ordered (solver.py:150-155)."""
+        if self.scheme != "hobi":
+            raise ValueError("singular partition exists only for scheme 'hobi'")
+        lo, hi = self.pair_starts[vertex], self.pair_starts[vertex + 1]
+        return self.pair_face[lo:hi]
+
+
+def discretize(mesh: FlatMesh, params: PhysicalParams, charges: ChargeSystem,
+               config: SolverConfig) -> DiscretizedProblem:
+    """Validate the mesh and build every cache on the GPU (solver.py:165-266)."""
+    mesh.validate()
+    N.require_device()
+    lib = N.load()
+    dev = _device_index()
+    v, n, f = N.f64(mesh.vertices), N.f64(mesh.normals), N.i64(mesh.faces)
+    ctx = C.c_void_p()
+    rule = config.regular_rule
+    duffy = duffy_rule(config.duffy_points)
+    if config.scheme == "hobi":
+        rpts, rw, rsh = N.f64(rule.points), N.f64(rule.weights), N.f64(shape_tables(rule.points))
+        dpts, dw, dsh = N.f64(duffy.points), N.f64(duffy.weights), N.f64(shape_tables(duffy.points))
+        st = lib.hobi_create(dev, N.dptr(v), N.dptr(n), mesh.n_vertices, N.iptr(f), mesh.n_faces,
+                             params.eps1, params.eps2, params.kappa, N.dptr(rpts), N.dptr(rw),
+                             N.dptr(rsh), len(rule), N.dptr(dpts), N.dptr(dw), N.dptr(dsh), len(duffy),
+                             C.byref(ctx))
+    else:
+        st = lib.hobi_create_lobi(dev, N.dptr(v), N.dptr(n), mesh.n_vertices, N.iptr(f), mesh.n_faces,
+                                  params.eps1, params.eps2, params.kappa, C.byref(ctx))
+    _raise(st)
+    handle = _Handle(ctx.value)
+    rank, world, _ = _world()
+    if world > 1:
+        _init_comm(handle.ptr, rank, world)
+    return DiscretizedProblem(mesh, params, charges, config.scheme, handle, rule, duffy, (rank, world))
+
+
+def _init_comm(ptr, rank, world):
+    """NCCL communicator for the row split; the unique id travels over torch.distributed."""
+    import torch.distributed as dist
+
+    lib = N.load()
+    uid = (C.c_ubyte * 128)()
+    if rank == 0:
+        _raise(lib.hobi_comm_unique_id(uid))
+    box = [bytes(uid) if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+    _raise(lib.hobi_comm_init(ptr, uid, world, rank))
+
+
+def _as_vector(problem, u):
+    u = N.f64(u)
+    T = problem.n_collocation
+    if u.shape != (2 * T,):
+        raise ValueError(f"expected vector of length {2 * T}, got shape {u.shape}")
+    return u
+
+
+def _full_matvec(problem: DiscretizedProblem, u) -> np.ndarray:
+    u = _as_vector(problem, u)
+    out = np.empty_like(u)
+    _raise(N.load().hobi_matvec(problem.handle, N.dptr(u), N.dptr(out)))
+    return out
+
+
+def matvec_hobi(problem: DiscretizedProblem, u) -> np.ndarray:
+    """Vertex-collocated curved-element operator (solver.py:379-383)."""
+    if problem.scheme != "hobi":
+        raise ValueError(f"problem was discretized for scheme {problem.scheme!r}")
+    return _full_matvec(problem, u)
+
+
+def matvec_lobi(problem: DiscretizedProblem, u) -> np.ndarray:
+    """Centroid-collocated flat-element operator (solver.py:386-390)."""
+    if problem.scheme != "lobi":
+        raise ValueError(f"problem was discretized for scheme {problem.scheme!r}")
+    return _full_matvec(problem, u)
+
+
+def apply_rows(problem: DiscretizedProblem, u, lo: int, hi: int):
+    """Rows [lo, hi) of both blocks (_apply_range, solver.py:278-367)."""
+    u = _as_vector(problem, u)
+    o1 = np.empty(max(hi - lo, 0))
+    o2 = np.empty(max(hi - lo, 0))
+    _raise(N.load().hobi_matvec_rows(problem.handle, N.dptr(u), lo, hi, N.dptr(o1), N.dptr(o2)))
+    return o1, o2
+
+
+def assemble_rhs(problem: DiscretizedProblem) -> np.ndarray:
+    """(S1, S2)/eps1 at the collocation points (solver.py:393-402)."""
+    q = N.f64(problem.charges.charges)
+    p = N.f64(problem.charges.positions)
+    b = np.empty(problem.n_unknowns)
+    _raise(N.load().hobi_rhs(problem.handle, N.dptr(p), N.dptr(q), q.size, N.dptr(b)))
+    return b
+
+
+def partition_targets(n_targets: int, n_workers: int) -> list[tuple[int, int]]:
+    """Contiguous ranges, sizes within 1 (solver.py:405-418)."""
+    if n_workers < 1:
+        raise ValueError(f"n_workers must be >= 1, got {n_workers}")
+    if n_targets < 0:
+        raise ValueError(f"n_targets must be >= 0, got {n_targets}")
+    base, extra = divmod(n_targets, n_workers)
+    out, lo = [], 0
+    for w in range(n_workers):
+        hi = lo + base + (1 if w < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+class GpuOperator:
+    """Callable matvec with the reference operator protocol (solver.py:432-472).
+
+    ``workers`` > 1 in a single process emulates that many row partitions on
+    one GPU (same gather layout and permutation kernel as the NCCL path).
+    """
+
+    def __init__(self, problem: DiscretizedProblem, workers: int = 1):
+        self._problem = problem
+        self._closed = False
+        if problem.world == 1 and workers > 1 and problem.n_collocation > 0:
+            _raise(N.load().hobi_emulate_ranks(problem.handle, workers))
+            self._emulated = True
+        else:
+            self._emulated = False
+
+    @property
+    def problem(self):
+        return self._problem
+
+    def __call__(self, u) -> np.ndarray:
+        if self._closed:
+            raise ValueError("operator is closed")
+        return _full_matvec(self._problem, u)
+
+    def close(self):
+        if self._emulated and not self._closed:
+            _raise(N.load().hobi_emulate_ranks(self._problem.handle, 1))
+        self._closed = True
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def make_operator(problem: DiscretizedProblem, config: SolverConfig) -> GpuOperator:
+    """Matvec closure honouring config.workers (solver.py:475-477)."""
+    return GpuOperator(problem, config.worker_count())
+
+
+def gmres_solve(apply, b, config: SolverConfig) -> SurfaceSolution:
+    """Restarted GMRES, true-residual restarts (solver.py:484-560), device-resident.
+
+    With a GpuOperator the whole solve runs in HBM (native matvec); any other
+    callable is applied through a host callback inside the same device GMRES.
+    """
+    b = N.f64(b)
+    n = b.size
+    if n % 2:
+        raise ValueError("vector length must be even: (phi, dphi/dn) halves")
+    N.require_device()
+    lib = N.load()
+    x = np.empty(n)
+    its, mv = C.c_int(0), C.c_int(0)
+    res, best = C.c_double(0.0), C.c_double(0.0)
+    if isinstance(apply, GpuOperator):
+        st = lib.hobi_gmres(apply.problem.handle, N.dptr(b), config.tolerance, config.restart,
+                            config.max_iterations, N.dptr(x), C.byref(its), C.byref(res), C.byref(best),
+                            C.byref(mv))
+    else:
+        err = []
+
+        def _cb(_user, src, dst, m):
+            try:
+                vin = np.ctypeslib.as_array(src, shape=(m,)).copy()
+                vout = np.asarray(apply(vin), dtype=float).reshape(m)
+                np.ctypeslib.as_array(dst, shape=(m,))[:] = vout
+                return 0
+            except Exception as exc:  # noqa: BLE001
+                err.append(exc)
+                return 1
+
+        cb = N.APPLY_FN(_cb)
+        st = lib.hobi_gmres_host_operator(_device_index(), n, cb, None, N.dptr(b), config.tolerance,
+                                          config.restart, config.max_iterations, N.dptr(x),
+                                          C.byref(its), C.byref(res), C.byref(best), C.byref(mv))
+        if err:
+            raise err[0]
+    if st == N.HOBI_ERR_NONCONVERGENCE:
+        raise GmresNonConvergence(N.last_error(), best_residual=best.value)
+    _raise(st)
+    half = n // 2
+    sol = SurfaceSolution(phi=x[:half], dphi_dn=x[half:], scheme=config.scheme,
+                          iterations=its.value, residual=res.value)
+    object.__setattr__(sol, "matvecs", mv.value)
+    return sol
+
+
+def solve(mesh: FlatMesh, params: PhysicalParams, charges: ChargeSystem,
+          config: SolverConfig) -> tuple[DiscretizedProblem, SurfaceSolution]:
+    """Discretize, assemble, and solve in one call (solver.py:563-574)."""
+    problem = discretize(mesh, params, charges, config)
+    b = assemble_rhs(problem)
+    with make_operator(problem, config) as op:
+        solution = gmres_solve(op, b, config)
+    return problem, solution
+
+
+def solvation_energy(problem: DiscretizedProblem, solution: SurfaceSolution) -> float:
+    """Reaction-field energy in kcal/mol (solver.py:581-614)."""
+    if len(problem.charges) == 0:
+        return 0.0
+    q = N.f64(problem.charges.charges)
+    p = N.f64(problem.charges.positions)
+    phi, dphi = N.f64(solution.phi), N.f64(solution.dphi_dn)
+    e = C.c_double(0.0)
+    _raise(N.load().hobi_energy(problem.handle, N.dptr(p), N.dptr(q), q.size, N.dptr(phi),
+                                N.dptr(dphi), C.byref(e)))
+    return float(e.value)
+
+
+def surface_potential_error(numerical, exact) -> float:
+    """max_i |num_i - exact_i| / max_i |exact_i| (solver.py:617-628)."""
+    numerical = np.asarray(numerical, dtype=float)
+    exact = np.asarray(exact, dtype=float)
+    if numerical.shape != exact.shape:
+        raise ValueError(f"shape mismatch: {numerical.shape} vs {exact.shape}")
+    scale = float(np.abs(exact).max())
+    if scale == 0.0:
+        raise ZeroDivisionError("exact vector is identically zero")
+    return float(np.abs(numerical - exact).max()) / scale
+
+
+def convergence_order(coarse_mesh: float, fine_mesh: float, coarse_error: float,
+                      fine_error: float) -> float:
+    """Observed order log(e_c/e_f) / |log(m_c/m_f)| (solver.py:631-655)."""
+    for name, value in (("coarse_mesh", coarse_mesh), ("fine_mesh", fine_mesh),
+                        ("coarse_error", coarse_error), ("fine_error", fine_error)):
+        if not value > 0.0:
+            raise ValueError(f"{name} must be positive, got {value}")
+    if coarse_mesh == fine_mesh:
+        raise ValueError("mesh parameters must differ")
+    return float(np.log(coarse_error / fine_error) / abs(np.log(coarse_mesh / fine_mesh)))
+
+
+__all__ = [
+    "DegenerateArcError", "DiscretizedProblem", "GmresNonConvergence", "GpuOperator", "SCHEMES",
+    "SolverConfig", "SurfaceSolution", "apply_rows", "assemble_rhs", "convergence_order",
+    "discretize", "gmres_solve", "make_operator", "matvec_hobi", "matvec_lobi", "partition_targets",
+    "solvation_energy", "solve", "surface_potential_error", "FOUR_PI", "KCAL_MOL_PER_E2_ANG",
+]

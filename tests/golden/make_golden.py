@@ -1,0 +1,146 @@
+"""Generate the golden fixtures under tests/golden/ by running the REFERENCE itself.
+
+Run once in the build container (the reference is importable only here):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every array in the .npz files comes out of the unmodified reference package
+``pbbem`` (solver.discretize / matvec_hobi / assemble_rhs / gmres_solve /
+solvation_energy, kernels.kernel_values_d, kirkwood.kirkwood_series); the
+inputs (meshes, charges, seeded vectors) come from this repo's generators and
+are stored alongside so the fixtures are self-contained on the GPU box.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from pbbem import kernels as rk  # noqa: E402
+from pbbem import solver as rs  # noqa: E402
+from pbbem.kirkwood import SphereProblem, kirkwood_series  # noqa: E402
+from pbbem.mesh import ChargeSystem as RCharges  # noqa: E402
+from pbbem.mesh import FlatMesh as RMesh  # noqa: E402
+
+from paper_1301_5914_b200.surfaces import StarShape, baseline_config  # noqa: E402
+
+
+def _ref_mesh(m):
+    return RMesh(vertices=m.vertices, normals=m.normals, faces=m.faces)
+
+
+def _ref_charges(c):
+    return RCharges(positions=c.positions, charges=c.charges)
+
+
+def _counted(op):
+    count = [0]
+
+    def apply(v):
+        count[0] += 1
+        return op(v)
+
+    return apply, count
+
+
+def case(name, mesh, charges, eps1, eps2, kappa, *, restart=None, caches=False, solve=False,
+         kirkwood_radius=None, u_seed=7, workers=8):
+    t0 = time.time()
+    params = rk.PhysicalParams(eps1, eps2, kappa)
+    cfg = rs.SolverConfig(scheme="hobi", workers=workers, restart=restart or 100)
+    prob = rs.discretize(_ref_mesh(mesh), params, _ref_charges(charges), cfg)
+    out = dict(vertices=mesh.vertices, normals=mesh.normals, faces=mesh.faces,
+               qpos=charges.positions, q=charges.charges,
+               params=np.array([eps1, eps2, kappa]))
+    u = np.random.default_rng(u_seed).standard_normal(prob.n_unknowns)
+    with rs.make_operator(prob, cfg) as op:
+        out["u"] = u
+        out["Au"] = op(u)
+        out["rhs"] = rs.assemble_rhs(prob)
+        if solve:
+            apply, count = _counted(op)
+            sol = rs.gmres_solve(apply, out["rhs"], cfg)
+            out["phi"], out["dphi"] = sol.phi, sol.dphi_dn
+            out["iterations"] = np.array(sol.iterations)
+            out["residual"] = np.array(sol.residual)
+            out["matvecs"] = np.array(count[0])
+            out["restart"] = np.array(cfg.restart)
+            out["energy"] = np.array(rs.solvation_energy(prob, sol))
+    if caches:
+        for k in ("reg_pos", "reg_nrm", "reg_w", "reg_bary", "pair_vertex", "pair_face",
+                  "pair_gverts", "pair_starts", "duf_pos", "duf_nrm", "duf_w", "duf_bary"):
+            out[k] = getattr(prob, k)
+    if kirkwood_radius is not None:
+        sph = SphereProblem(radius=kirkwood_radius, params=params, charges=_ref_charges(charges))
+        ks = kirkwood_series(sph, n_terms=40)
+        out["kirkwood_energy"] = np.array(ks.energy)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(f"{name}: N_v={mesh.n_vertices} N_f={mesh.n_faces} {time.time() - t0:.1f}s", flush=True)
+
+
+def kernel_table():
+    """kernels.kernel_values_d on random pairs, incl. near-coincident and kappa = 0."""
+    rng = np.random.default_rng(11)
+    n = 4000
+    d = rng.standard_normal((n, 3)) * np.exp(rng.uniform(np.log(1e-3), np.log(60.0), n))[:, None]
+    nx = rng.standard_normal((n, 3))
+    nx /= np.linalg.norm(nx, axis=1)[:, None]
+    ny = rng.standard_normal((n, 3))
+    ny /= np.linalg.norm(ny, axis=1)[:, None]
+    out = dict(d=d, nx=nx, ny=ny)
+    for tag, (e1, e2, kap) in {"a": (1.0, 80.0, 0.1257), "b": (2.0, 80.0, 0.5),
+                               "c": (4.0, 80.0, 0.0), "d": (3.0, 3.0, 0.0)}.items():
+        ks = rk.kernel_values_d(d, nx, ny, rk.PhysicalParams(e1, e2, kap))
+        out["params_" + tag] = np.array([e1, e2, kap])
+        out["K_" + tag] = np.stack(ks, axis=0)
+    np.savez_compressed(os.path.join(HERE, "kernels.npz"), **out)
+    print("kernels: done", flush=True)
+
+
+def degenerate_case():
+    """The reference's first-failing-face error (test_solver.py:109-115 octahedron)."""
+    verts = np.array([[1.0, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]])
+    faces = np.array([[0, 2, 4], [2, 1, 4], [1, 3, 4], [3, 0, 4], [2, 0, 5], [1, 2, 5],
+                      [3, 1, 5], [0, 3, 5]])
+    normals = verts.copy()
+    normals[0] = np.array([-1.0, 1.0, 0.0]) / np.sqrt(2.0)
+    try:
+        rs.discretize(RMesh(vertices=verts, normals=normals, faces=faces),
+                      rk.PhysicalParams(1.0, 80.0, 0.0),
+                      RCharges(positions=np.zeros((0, 3)), charges=np.zeros(0)),
+                      rs.SolverConfig(scheme="hobi"))
+        msg = ""
+    except Exception as exc:  # noqa: BLE001
+        msg = f"{type(exc).__name__}: {exc}"
+    np.savez_compressed(os.path.join(HERE, "degenerate.npz"), vertices=verts, normals=normals,
+                        faces=faces, message=np.array(msg))
+    print("degenerate:", msg, flush=True)
+
+
+def main():
+    kernel_table()
+    degenerate_case()
+    star = StarShape.from_seed(16.0, seed=3)
+    few = star.interior_charges(50, seed=4)
+    from paper_1301_5914_b200.mesh import ChargeSystem, icosahedral_sphere
+
+    centred = ChargeSystem(positions=[[0.0, 0.0, 0.0]], charges=[1.0])
+    case("sphere_l1_mixed", icosahedral_sphere(1, 2.0), centred, 2.0, 80.0, 0.5, caches=True)
+    case("star_l2", star.surface(2), few, 2.0, 80.0, 0.1257, restart=20, caches=True, solve=True)
+    case("star_l3", star.surface(3), few, 2.0, 80.0, 0.1257, restart=20, solve=True)
+    c1 = baseline_config(1)
+    case("c1", c1.mesh, c1.charges, c1.eps1, c1.eps2, c1.kappa, restart=c1.restart, solve=True,
+         kirkwood_radius=2.0)
+    c2 = baseline_config(2)
+    case("c2", c2.mesh, c2.charges, c2.eps1, c2.eps2, c2.kappa, restart=c2.restart, solve=True,
+         kirkwood_radius=2.0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (tests/golden, produced by running pbbem itself) and the numpy oracle.
+
+Tolerances (north star, BASELINE.json): matvec <= 1e-10 relative L2 (we hold
+1e-12); potentials and energy <= 1e-8 relative at equal GMRES tolerance;
+geometry caches bit-exact (the device geometry replays numpy's rounding).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_1301_5914_b200")
+from paper_1301_5914_b200 import (  # noqa: E402
+    ChargeSystem,
+    DegenerateArcError,
+    FlatMesh,
+    GmresNonConvergence,
+    PhysicalParams,
+    SolverConfig,
+    apply_rows,
+    assemble_rhs,
+    discretize,
+    gmres_solve,
+    make_operator,
+    matvec_hobi,
+    matvec_lobi,
+    solvation_energy,
+    solve,
+)
+from paper_1301_5914_b200 import _native as N  # noqa: E402
+
+MATVEC_TOL = 1e-12
+SOLVE_TOL = 1e-8
+
+
+def _problem(g, scheme="hobi", **kw):
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    e1, e2, k = g["params"]
+    charges = ChargeSystem(g["qpos"], g["q"])
+    return discretize(mesh, PhysicalParams(e1, e2, k), charges,
+                      SolverConfig(scheme=scheme, workers=1, **kw))
+
+
+def test_kernel_values_match_reference():
+    """Device kernel_values_d vs kernels.kernel_values_d (kernels.py:99-130)."""
+    g = golden("kernels")
+    n = g["d"].shape[0]
+    for tag in "abcd":
+        e1, e2, kap = g["params_" + tag]
+        k = np.empty((4, n))
+        N.check(N.load().hobi_kernel_values(0, N.dptr(N.f64(g["d"])), N.dptr(N.f64(g["nx"])),
+                                            N.dptr(N.f64(g["ny"])), n, e1, e2, kap, N.dptr(k)))
+        ref = g["K_" + tag]
+        kr = kap * np.linalg.norm(g["d"], axis=1)
+        # K2..K4 carry the O((kr)^2) cancellations a, b of kernels.py:117-120,
+        # whose rounding (either implementation) grows like ulp/kr.
+        bound = [np.full(n, 1e-14), np.full(n, 1e-13), np.full(n, 1e-13),
+                 1e-14 * (1.0 + 1.0 / np.maximum(kr, 1e-300))]
+        for i in range(4):
+            nz = ref[i] != 0.0
+            assert np.all(k[i][~nz] == 0.0)  # identity medium / kappa=0: exact zeros
+            err = np.abs(k[i][nz] - ref[i][nz]) / np.abs(ref[i][nz])
+            assert np.all(err <= bound[i][nz]), (tag, i, err.max())
+
+
+@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2"])
+def test_geometry_caches_bit_exact(name):
+    g = golden(name)
+    prob = _problem(g)
+    for key in ("reg_pos", "reg_nrm", "reg_w", "duf_pos", "duf_nrm", "duf_w"):
+        got, ref = getattr(prob, key), g[key]
+        assert got.shape == ref.shape
+        assert np.array_equal(got, ref), (key, np.abs(got - ref).max())
+    for key in ("pair_vertex", "pair_face", "pair_gverts", "pair_starts"):
+        assert np.array_equal(getattr(prob, key), g[key]), key
+
+
+@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "star_l3", "c1", "c2"])
+def test_matvec_matches_reference(name):
+    g = golden(name)
+    prob = _problem(g)
+    got = matvec_hobi(prob, g["u"])
+    assert rel_l2(got, g["Au"]) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "star_l3", "c1", "c2"])
+def test_rhs_matches_reference(name):
+    g = golden(name)
+    prob = _problem(g)
+    assert rel_l2(assemble_rhs(prob), g["rhs"]) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["star_l2", "star_l3", "c1", "c2"])
+def test_solve_matches_reference(name):
+    g = golden(name)
+    prob = _problem(g, restart=int(g["restart"]))
+    cfg = SolverConfig(workers=1, restart=int(g["restart"]))
+    with make_operator(prob, cfg) as op:
+        sol = gmres_solve(op, assemble_rhs(prob), cfg)
+    assert sol.iterations == int(g["iterations"])
+    assert sol.matvecs == int(g["matvecs"])
+    assert rel_l2(sol.phi, g["phi"]) <= SOLVE_TOL
+    assert rel_l2(sol.dphi_dn, g["dphi"]) <= SOLVE_TOL
+    e = solvation_energy(prob, sol)
+    assert abs(e - float(g["energy"])) <= SOLVE_TOL * abs(float(g["energy"]))
+    if "kirkwood_energy" in g:  # analytic sphere answer, HOBI discretisation error ~1e-3
+        assert abs(e - float(g["kirkwood_energy"])) <= 5e-3 * abs(float(g["kirkwood_energy"]))
+
+
+def test_identity_medium_is_exact_identity():
+    """eps1 = eps2, kappa = 0: every kernel vanishes, operator == I bitwise (test_solver.py:138-148)."""
+    g = golden("star_l2")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    rng = np.random.default_rng(0)
+    for scheme, apply in (("hobi", matvec_hobi), ("lobi", matvec_lobi)):
+        prob = discretize(mesh, PhysicalParams(3.0, 3.0, 0.0), ChargeSystem(np.zeros((0, 3)), []),
+                          SolverConfig(scheme=scheme))
+        for _ in range(5):
+            u = rng.standard_normal(prob.n_unknowns)
+            assert np.abs(apply(prob, u) - u).max() == 0.0
+
+
+def test_row_split_bitwise_deterministic():
+    """Any partition of rows reproduces the unsplit operator bitwise (test_solver.py:333-359)."""
+    g = golden("star_l3")
+    prob = _problem(g)
+    u = g["u"]
+    full = matvec_hobi(prob, u)
+    T = prob.n_collocation
+    for workers in (2, 3, 4, 8, 700):
+        with make_operator(prob, SolverConfig(workers=workers)) as op:
+            assert np.array_equal(op(u), full), workers
+        from paper_1301_5914_b200 import partition_targets
+
+        parts = [apply_rows(prob, u, lo, hi) for lo, hi in partition_targets(T, workers)]
+        assert np.array_equal(np.concatenate([p[0] for p in parts]), full[:T])
+        assert np.array_equal(np.concatenate([p[1] for p in parts]), full[T:])
+
+
+def test_degenerate_face_reported_like_reference():
+    g = golden("degenerate")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    with pytest.raises(DegenerateArcError) as info:
+        discretize(mesh, PhysicalParams(1.0, 80.0, 0.0), ChargeSystem(np.zeros((0, 3)), []),
+                   SolverConfig(scheme="hobi"))
+    assert f"DegenerateArcError: {info.value}" == str(g["message"])
+
+
+def test_gmres_host_callable_paths():
+    """gmres_solve on arbitrary callables (test_solver.py:246-297)."""
+    rng = np.random.default_rng(3)
+    a = np.eye(8) + 0.3 * rng.standard_normal((8, 8))
+    b = rng.standard_normal(8)
+    sol = gmres_solve(lambda v: a @ v, b, SolverConfig(tolerance=1e-12, workers=1))
+    assert np.abs(sol.vector - np.linalg.solve(a, b)).max() <= 1e-9
+    assert sol.iterations <= 8 and sol.residual <= 1e-12
+    rng = np.random.default_rng(4)
+    a = np.eye(12) + 0.1 * rng.standard_normal((12, 12))
+    b = rng.standard_normal(12)
+    sol = gmres_solve(lambda v: a @ v, b, SolverConfig(tolerance=1e-12, restart=3, max_iterations=500))
+    assert np.abs(a @ sol.vector - b).max() <= 1e-10 and sol.iterations > 3
+    b = np.array([1.0, -2.0, 0.5, 3.0])
+    sol = gmres_solve(lambda v: v, b, SolverConfig())
+    assert np.array_equal(sol.vector, b) and sol.iterations == 1
+    sol = gmres_solve(lambda v: v, np.zeros(6), SolverConfig())
+    assert np.all(sol.vector == 0.0) and sol.iterations == 0 and sol.residual == 0.0
+    with pytest.raises(ValueError, match="even"):
+        gmres_solve(lambda v: v, np.ones(5), SolverConfig())
+    rng = np.random.default_rng(5)
+    a = np.eye(20) + 2.5 * rng.standard_normal((20, 20))
+    with pytest.raises(GmresNonConvergence) as info:
+        gmres_solve(lambda v: a @ v, rng.standard_normal(20),
+                    SolverConfig(tolerance=1e-14, max_iterations=3))
+    assert 0.0 < info.value.best_residual <= 1.0
+
+
+def test_gmres_matches_oracle_gmres_on_dense():
+    import hobi_oracle as O
+
+    rng = np.random.default_rng(9)
+    a = np.eye(40) + 0.05 * rng.standard_normal((40, 40))
+    b = rng.standard_normal(40)
+    x, its, rel, nmv = O.gmres(lambda v: a @ v, b, tol=1e-10, restart=7, max_it=400)
+    sol = gmres_solve(lambda v: a @ v, b, SolverConfig(tolerance=1e-10, restart=7, max_iterations=400))
+    assert sol.iterations == its and sol.matvecs == nmv
+    assert rel_l2(sol.vector, x) <= 1e-12
+
+
+def test_lobi_matches_oracle():
+    import hobi_oracle as O
+
+    g = golden("star_l2")
+    prob = _problem(g, scheme="lobi")
+    o = O.discretize(g["vertices"], g["normals"], g["faces"], *g["params"], scheme="lobi")
+    rng = np.random.default_rng(2)
+    u = rng.standard_normal(prob.n_unknowns)
+    assert rel_l2(matvec_lobi(prob, u), O.matvec(o, u)) <= MATVEC_TOL
+    assert rel_l2(assemble_rhs(prob), O.rhs(O.discretize(
+        g["vertices"], g["normals"], g["faces"], *g["params"], g["qpos"], g["q"], scheme="lobi"))) <= 1e-14
+
+
+def test_born_sphere_frozen_energy():
+    """Known answer of the reference test-suite (test_solver.py:375-392)."""
+    from paper_1301_5914_b200 import icosahedral_sphere
+
+    water = PhysicalParams(1.0, 80.0, 0.0)
+    prob, sol = solve(icosahedral_sphere(2, 2.0), water, ChargeSystem([[0.0, 0.0, 0.0]], [1.0]),
+                      SolverConfig(workers=1))
+    assert solvation_energy(prob, sol) == pytest.approx(-81.98131581725495, rel=1e-9)
+    assert 4 <= sol.iterations <= 9
+    prob, sol = solve(icosahedral_sphere(2, 2.0), water, ChargeSystem([[0.0, 0.0, 0.0]], [1.0]),
+                      SolverConfig(scheme="lobi", workers=1))
+    assert solvation_energy(prob, sol) == pytest.approx(-86.3199784371863, rel=1e-9)
+
+
+@pytest.mark.parametrize("index", [3, 4])
+def test_large_config_rows_vs_oracle(index):
+    """Configs 3-4 at full size: sampled rows against the oracle's _apply_range."""
+    import hobi_oracle as O
+    from paper_1301_5914_b200.surfaces import baseline_config
+
+    cfg = baseline_config(index)
+    prob = discretize(cfg.mesh, PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa), cfg.charges,
+                      SolverConfig(workers=1))
+    o = O.discretize(cfg.mesh.vertices, cfg.mesh.normals, cfg.mesh.faces, cfg.eps1, cfg.eps2,
+                     cfg.kappa, check=False)
+    u = np.random.default_rng(0).standard_normal(prob.n_unknowns)
+    full = matvec_hobi(prob, u)
+    T = prob.n_collocation
+    for lo in (0, T // 2, T - 37):
+        hi = lo + 37
+        r1, r2 = O.rows(o, u, lo, hi)
+        assert rel_l2(full[lo:hi], r1) <= MATVEC_TOL
+        assert rel_l2(full[T + lo:T + hi], r2) <= MATVEC_TOL
