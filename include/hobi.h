@@ -145,8 +145,25 @@ int hobi_emulate_ranks(hobi_ctx* ctx, int nranks);
  * and the count of every kernel this library launched. */
 int hobi_timing_reset(hobi_ctx* ctx);
 int hobi_timing(hobi_ctx* ctx, double* sweep_ms, int64_t* sweep_launches, int64_t* all_launches);
+/* Tuning hook: select all-pairs sweep variant `variant` (< 0 keeps the
+ * current one); reports the number of variants and the active one's name. */
+int hobi_sweep_variant(hobi_ctx* ctx, int variant, int* count, char* name, int name_len);
+
 /* Regular pairs per full matvec (N_v x N_f x nq for hobi), for throughput. */
 int hobi_pairs_per_matvec(hobi_ctx* ctx, double* pairs);
+
+/*
+ * Benchmark helper: `steps` operator applications, each bracketed by CUDA
+ * events on the context stream; ms[i] receives step i's device time.
+ * mode 0: u is copied to HBM once before the loop, each step is
+ *         HBM-resident u -> A u (the kernel-level `value`);
+ * mode 1: each step is the host-buffer call of hobi_matvec: H2D of u,
+ *         operator, D2H of A u (the end-to-end `e2e`).
+ * flush_l2 != 0 writes a 512 MiB scratch buffer between steps (outside the
+ * brackets) so no step starts with the previous step's data in L2.
+ */
+int hobi_bench(hobi_ctx* ctx, const double* u, double* out, int steps, int mode, int flush_l2,
+               double* ms);
 
 /* DFMA throughput probe (FP64 roofline denominator), TFLOP/s over ~`ms` ms. */
 int hobi_probe_fp64_tflops(int device, double ms, double* tflops);

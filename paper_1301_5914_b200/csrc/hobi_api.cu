@@ -353,6 +353,7 @@ int hobi_destroy(hobi_ctx* c) {
   cudaSetDevice(c->device);
   if (c->comm.nccl && nccl::api().loaded) nccl::api().destroy(c->comm.nccl);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   cudaStream_t s = c->stream;
@@ -556,6 +557,8 @@ int hobi_emulate_ranks(hobi_ctx* c, int nranks) {
 
 int hobi_timing_reset(hobi_ctx* c) {
   if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  if (collect_sweep_timing(c)) return HOBI_ERR_CUDA;
   c->sweep_ms = 0.0;
   c->sweep_launches = 0;
   c->launches = 0;
@@ -564,9 +567,60 @@ int hobi_timing_reset(hobi_ctx* c) {
 
 int hobi_timing(hobi_ctx* c, double* sweep_ms, int64_t* sweep_launches, int64_t* all_launches) {
   if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  if (collect_sweep_timing(c)) return HOBI_ERR_CUDA;
   if (sweep_ms) *sweep_ms = c->sweep_ms;
   if (sweep_launches) *sweep_launches = c->sweep_launches;
   if (all_launches) *all_launches = c->launches;
+  return 0;
+}
+
+int hobi_bench(hobi_ctx* c, const double* u, double* out, int steps, int mode, int flush_l2,
+               double* ms) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (steps < 0 || (mode != 0 && mode != 1)) return fail(HOBI_ERR_VALUE, "bad bench arguments");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  const size_t bytes = 2 * c->nt * sizeof(double);
+  DevBuf<unsigned char> scratch;
+  const size_t flush_bytes = (size_t)512 << 20;
+  if (flush_l2 && scratch.alloc(flush_bytes)) return HOBI_ERR_CUDA;
+  cudaEvent_t e0, e1;
+  HOBI_CUDA(cudaEventCreate(&e0));
+  HOBI_CUDA(cudaEventCreate(&e1));
+  int rc = 0;
+  if (mode == 0) HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, bytes, cudaMemcpyHostToDevice, c->stream));
+  for (int i = 0; i < steps && !rc; ++i) {
+    if (flush_l2) HOBI_CUDA(cudaMemsetAsync(scratch.p, i & 0xff, flush_bytes, c->stream));
+    HOBI_CUDA(cudaEventRecord(e0, c->stream));
+    if (mode == 1) HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, bytes, cudaMemcpyHostToDevice, c->stream));
+    rc = matvec_full_device(c, c->u.p, c->out.p);
+    if (rc) break;
+    if (mode == 1) HOBI_CUDA(cudaMemcpyAsync(out, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    HOBI_CUDA(cudaEventRecord(e1, c->stream));
+    HOBI_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    HOBI_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    ms[i] = t;
+  }
+  if (!rc && mode == 0 && out) {
+    HOBI_CUDA(cudaMemcpyAsync(out, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return rc;
+}
+
+int hobi_sweep_variant(hobi_ctx* c, int variant, int* count, char* name, int name_len) {
+  if (count) *count = sweep_variant_count();
+  if (!c) return 0;
+  if (variant >= 0) {
+    if (variant >= sweep_variant_count()) return fail(HOBI_ERR_VALUE, "no such sweep variant");
+    c->sweep_variant = variant;
+  }
+  if (name && name_len > 0) {
+    snprintf(name, name_len, "%s", sweep_variant_name(c->sweep_variant));
+  }
   return 0;
 }
 

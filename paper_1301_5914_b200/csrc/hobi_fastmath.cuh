@@ -3,11 +3,13 @@
 // coordinates are pre-scaled by kappa so r' = kappa*r, the physical constants
 // (1/4pi, kappa^n, er, 1/er) are folded into six per-source weights, expm1 and
 // exp share one table-driven range reduction, and 1/r comes from the MUFU
-// rsqrt seed plus one third-order Newton step.  50 FP64 instructions per pair
+// rsqrt seed plus one third-order Newton step.  48 FP64 instructions per pair
 // (vs ~95 for a literal libdevice transcription of kernels.py:112-130).
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include "hobi_internal.cuh"
 
 namespace hobi {
 
@@ -23,24 +25,23 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   return fma(ye, c, y);
 }
 
-// exp(-x) - 1 for 0 <= x < 1e12, computed as S(1+p) - 1 with S = 2^(k/256)
-// from a 256-entry table (shared memory) and p = e^f - 1 on |f| <= ln2/512
-// (degree-4 Taylor, truncation < 4e-17).  S - 1 is exact for S in [1/2, 1]
-// (Sterbenz), so small arguments keep expm1's relative accuracy.
+// exp(-x) - 1 for 0 <= x < 1e12, computed as S(1+p) - 1 with S = 2^(k/2048)
+// from a 2048-entry table (shared memory) and p = e^f - 1 on |f| <= ln2/4096
+// (degree-3 Taylor, truncation < 4e-17).  S - 1 is exact for S in [1/2, 1]
+// (Sterbenz), so small arguments keep expm1's relative accuracy.  8 FP64 ops.
 __device__ __forceinline__ double expm1_neg(double x, const double* __restrict__ etab) {
-  const double kInv = 369.32993046757463;      // 256/ln2
+  const double kInv = 2954.6394437405970;      // 2048/ln2
   const double kMagic = 6755399441055744.0;    // 1.5*2^52: rounds to integer in the low word
-  const double kStep = 2.7076061740622863e-3;  // ln2/256
+  const double kStep = 3.3845077175778578e-4;  // ln2/2048
   double kf = fma(-x, kInv, kMagic);
   int k = __double2loint(kf);
   double kd = kf - kMagic;
   double f = fma(kd, -kStep, -x);
-  double p = fma(f, 4.1666666666666664e-2, 1.6666666666666666e-1);
-  p = fma(p, f, 0.5);
+  double p = fma(f, 1.6666666666666666e-1, 0.5);
   p = fma(p, f, 1.0);
   p = p * f;
-  double T = etab[k & 255];
-  int n = k >> 8;
+  double T = etab[k & (kExpTable - 1)];
+  int n = k >> kExpShift;
   double S = __hiloint2double(__double2hiint(T) + (n << 20), __double2loint(T));
   S = (n < -1000) ? 0.0 : S;
   return fma(S, p, S - 1.0);
@@ -72,12 +73,13 @@ __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, d
   if (FULL) {
     double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
     double nn = fma(nx, mx, fma(ny, my, nz * mz));
-    acc2 = fma(dnx * ir3, fma(a, C, D), acc2);    // K3 wd
-    // K4 wp: b = 3a + kr*kre (kernels.py:120), K4 ~ a nn - b Q with Q = dnx dny / r^2
+    // K3 wd + K4 wp = ir3 (dnx (a C + D) + W4 (a P - z)), with b = 3a + kr*kre
+    // (kernels.py:120) folded as a nn - b Q = a (nn - 3Q) - kr kre Q, Q = dnx dny / r^2
     double Q = (dnx * dny) * ir2;
     double P = fma(Q, -3.0, nn);
     double z = (r * kre) * Q;
-    acc2 = fma(ir3 * W4, fma(a, P, -z), acc2);
+    double k4 = W4 * fma(a, P, -z);
+    acc2 = fma(ir3, fma(dnx, fma(a, C, D), k4), acc2);
   }
 }
 

@@ -21,7 +21,8 @@ constexpr int kTargetTile = kSweepThreads * kSweepR;
 constexpr int kSrcTile = 64;        // sources per shared-memory stage
 constexpr int kSrcStride = 12;      // doubles per source record
 constexpr int kStages = 4;          // TMA bulk-copy pipeline depth
-constexpr int kExpTable = 256;      // 2^(j/256) table for the FP64 exp
+constexpr int kExpShift = 11;
+constexpr int kExpTable = 1 << kExpShift;  // 2^(j/2048) table for the FP64 exp
 
 enum Scheme { kHobi = 0, kLobi = 1 };
 enum KernelMode { kLaplace = 0, kScreened = 1 };
@@ -112,10 +113,13 @@ struct hobi_ctx {
 
   // instrumentation
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> ev_pool;   // recorded sweep brackets, read lazily
+  size_t ev_used = 0;                  // pairs of ev_pool in flight
   double sweep_ms = 0.0;
   int64_t sweep_launches = 0;
   int64_t launches = 0;
   bool timing = true;
+  int sweep_variant = 4;  // index into the sweep tuning table (hobi_sweep.cu): R4_minb3_unroll1
 };
 
 namespace hobi {
@@ -127,6 +131,9 @@ int build_geometry(hobi_ctx* c, const int* pair_of_slot, int* first_bad_slot, in
 
 // sweep (hobi_sweep.cu)
 int upload_exp_table();
+int collect_sweep_timing(hobi_ctx* c);
+int sweep_variant_count();
+const char* sweep_variant_name(int v);
 int prepare_targets(hobi_ctx* c);
 int prepare_static_sources(hobi_ctx* c);
 int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi, double* o1,

@@ -72,8 +72,8 @@ constexpr uint32_t kTileBytes = kSrcTile * kSrcStride * sizeof(double);
 constexpr size_t kSweepSmem =
     (size_t)kStages * kTileBytes + kExpTable * sizeof(double) + kStages * sizeof(uint64_t);
 
-template <int MODE, bool FULL, bool SELF>
-__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
+template <int MODE, bool FULL, bool SELF, int R, int MINB, int UNROLL>
+__global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
     const double* __restrict__ tgt, int64_t ldt, int64_t t_begin, int64_t t_end,
     const double* __restrict__ src, int n_src_tiles, int tiles_per_group, double* __restrict__ part,
     int64_t ldp) {
@@ -85,12 +85,12 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
   const int g = blockIdx.y;
   const int tile0 = g * tiles_per_group;
   const int ntl = min(tiles_per_group, n_src_tiles - tile0);
-  const int64_t tb = t_begin + (int64_t)blockIdx.x * kTargetTile + threadIdx.x;
+  const int64_t tb = t_begin + (int64_t)blockIdx.x * (kSweepThreads * R) + threadIdx.x;
 
-  double tx[kSweepR], ty[kSweepR], tz[kSweepR], nx[kSweepR], ny[kSweepR], nz[kSweepR];
-  double a1[kSweepR], a2[kSweepR];
+  double tx[R], ty[R], tz[R], nx[R], ny[R], nz[R];
+  double a1[R], a2[R];
 #pragma unroll
-  for (int q = 0; q < kSweepR; ++q) {
+  for (int q = 0; q < R; ++q) {
     int64_t t = min(tb + q * kSweepThreads, t_end - 1);  // padded threads recompute the last row
     tx[q] = tgt[t];
     ty[q] = tgt[ldt + t];
@@ -128,12 +128,12 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     const int s = it % kStages;
     mbar_wait(&bars[s], (uint32_t)((it / kStages) & 1));
     const double2* rec = reinterpret_cast<const double2*>(ring + s * kSrcTile * kSrcStride);
-#pragma unroll 2
+#pragma unroll UNROLL
     for (int j = 0; j < kSrcTile; ++j) {
       const double2 p01 = rec[6 * j + 0], p2m0 = rec[6 * j + 1], m12 = rec[6 * j + 2];
       double2 w01 = rec[6 * j + 3], w23 = rec[6 * j + 4], w45 = rec[6 * j + 5];
 #pragma unroll
-      for (int q = 0; q < kSweepR; ++q) {
+      for (int q = 0; q < R; ++q) {
         double sx = p01.x, sy = p01.y, sz = p2m0.x;
         if (SELF) {
           // LOBI self pair: displacement forced to (1,0,0) and weights to 0, so
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     __syncthreads();
   }
 #pragma unroll
-  for (int q = 0; q < kSweepR; ++q) {
+  for (int q = 0; q < R; ++q) {
     int64_t t = tb + q * kSweepThreads;
     if (t < t_end) {
       part[(2 * (int64_t)g) * ldp + t] = a1[q];
@@ -303,35 +303,85 @@ __global__ void energy_reduce_kernel(const double* __restrict__ part, int64_t ld
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+}  // namespace
+
+int collect_sweep_timing(hobi_ctx* c) {
+  for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
+    HOBI_CUDA(cudaEventSynchronize(c->ev_pool[k + 1]));
+    float ms = 0.f;
+    HOBI_CUDA(cudaEventElapsedTime(&ms, c->ev_pool[k], c->ev_pool[k + 1]));
+    c->sweep_ms += ms;
+    c->sweep_launches++;
+  }
+  c->ev_used = 0;
+  return 0;
+}
+
+namespace {
+
+typedef void (*SweepFn)(const double*, int64_t, int64_t, int64_t, const double*, int, int, double*,
+                        int64_t);
+
+struct SweepVariant {
+  SweepFn fn;
+  int r;  // targets per thread
+  const char* name;
+};
+
+// Tuning variants of the hot instantiation (screened, full, no self mask):
+// targets per thread x min CTAs per SM (register cap) x source unroll.
+#define HOBI_V(R, M, U) \
+  { sweep_kernel<kScreened, true, false, R, M, U>, R, "R" #R "_minb" #M "_unroll" #U }
+static const SweepVariant kVariants[] = {
+    HOBI_V(2, 1, 2), HOBI_V(2, 6, 2), HOBI_V(2, 8, 2), HOBI_V(1, 8, 2), HOBI_V(4, 3, 1),
+    HOBI_V(4, 4, 1), HOBI_V(3, 4, 1), HOBI_V(2, 1, 1), HOBI_V(2, 6, 1), HOBI_V(1, 8, 4),
+};
+#undef HOBI_V
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
 int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_t t1, bool full,
                  double* part, int64_t ldp, int n_groups, int tiles_per_group) {
   if (t1 <= t0) return 0;
-  dim3 grid(nblk(t1 - t0, kTargetTile), n_groups);
   const bool self = c->scheme == kLobi && full;
-  void (*fn)(const double*, int64_t, int64_t, int64_t, const double*, int, int, double*, int64_t);
-  if (c->phys.mode == kScreened)
-    fn = self ? sweep_kernel<kScreened, true, true>
-              : (full ? sweep_kernel<kScreened, true, false> : sweep_kernel<kScreened, false, false>);
-  else
-    fn = self ? sweep_kernel<kLaplace, true, true>
-              : (full ? sweep_kernel<kLaplace, true, false> : sweep_kernel<kLaplace, false, false>);
-  static bool attr_done[2][2][2] = {};
-  if (!attr_done[c->phys.mode][full][self]) {
-    HOBI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
-    attr_done[c->phys.mode][full][self] = true;
+  SweepFn fn;
+  int r = kSweepR;
+  if (c->phys.mode == kScreened) {
+    if (self)
+      fn = sweep_kernel<kScreened, true, true, kSweepR, 1, 2>;
+    else if (full) {
+      const SweepVariant& v = kVariants[c->sweep_variant];
+      fn = v.fn;
+      r = v.r;
+    } else
+      fn = sweep_kernel<kScreened, false, false, kSweepR, 1, 2>;
+  } else {
+    fn = self ? sweep_kernel<kLaplace, true, true, kSweepR, 1, 2>
+              : (full ? sweep_kernel<kLaplace, true, false, kSweepR, 1, 2>
+                      : sweep_kernel<kLaplace, false, false, kSweepR, 1, 2>);
   }
-  if (c->timing) HOBI_CUDA(cudaEventRecord(c->ev0, c->stream));
+  HOBI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
+  dim3 grid(nblk(t1 - t0, kSweepThreads * r), n_groups);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {  // brackets are read lazily by collect_sweep_timing: no sync here
+    if (c->ev_used + 2 > c->ev_pool.size()) {
+      for (int k = 0; k < 2; ++k) {
+        cudaEvent_t e;
+        HOBI_CUDA(cudaEventCreate(&e));
+        c->ev_pool.push_back(e);
+      }
+    }
+    e0 = c->ev_pool[c->ev_used];
+    e1 = c->ev_pool[c->ev_used + 1];
+    c->ev_used += 2;
+    HOBI_CUDA(cudaEventRecord(e0, c->stream));
+  }
   fn<<<grid, kSweepThreads, kSweepSmem, c->stream>>>(tgt, ldt, t0, t1, c->src.p, c->n_src_tiles,
                                                      tiles_per_group, part, ldp);
   HOBI_CUDA(cudaGetLastError());
   c->launches++;
   if (c->timing) {
-    HOBI_CUDA(cudaEventRecord(c->ev1, c->stream));
-    HOBI_CUDA(cudaEventSynchronize(c->ev1));
-    float ms = 0.f;
-    HOBI_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    c->sweep_ms += ms;
-    c->sweep_launches++;
+    HOBI_CUDA(cudaEventRecord(e1, c->stream));
+    if (c->ev_used >= 256 && collect_sweep_timing(c)) return HOBI_ERR_CUDA;
   }
   return 0;
 }
@@ -350,6 +400,9 @@ void weight_constants(const Physics& p, double* kA, double* kB, double* kC, doub
 }
 
 }  // namespace
+
+int sweep_variant_count() { return kNumVariants; }
+const char* sweep_variant_name(int v) { return (v >= 0 && v < kNumVariants) ? kVariants[v].name : ""; }
 
 int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1);  // hobi_literal.cu
 

@@ -55,16 +55,26 @@ def test_kernel_values_match_reference():
         N.check(N.load().hobi_kernel_values(0, N.dptr(N.f64(g["d"])), N.dptr(N.f64(g["nx"])),
                                             N.dptr(N.f64(g["ny"])), n, e1, e2, kap, N.dptr(k)))
         ref = g["K_" + tag]
-        kr = kap * np.linalg.norm(g["d"], axis=1)
-        # K2..K4 carry the O((kr)^2) cancellations a, b of kernels.py:117-120,
-        # whose rounding (either implementation) grows like ulp/kr.
-        bound = [np.full(n, 1e-14), np.full(n, 1e-13), np.full(n, 1e-13),
-                 1e-14 * (1.0 + 1.0 / np.maximum(kr, 1e-300))]
+        d, nx, ny = g["d"], g["nx"], g["ny"]
+        r2 = np.einsum("ij,ij->i", d, d)
+        r = np.sqrt(r2)
+        kr = kap * r
+        a = np.expm1(-kr) + kr * np.exp(-kr)
+        b = 3.0 * np.expm1(-kr) + kr * np.exp(-kr) * (3.0 + kr)
+        dnx, dny = np.einsum("ij,ij->i", d, nx), np.einsum("ij,ij->i", d, ny)
+        inv3 = 1.0 / (4.0 * np.pi * r2 * r)
+        # a, b are O((kr)^2) cancellations (kernels.py:117-120): any implementation's
+        # rounding in them is ~ulp/kr relative, then K4 adds the cancellation
+        # between its two terms; bound the error by the terms' magnitudes.
+        cond = 1.0 + 1.0 / np.maximum(kr, 1e-300)
+        k4_scale = (np.abs(b * dnx * dny / r2) + np.abs(a * np.einsum("ij,ij->i", nx, ny))) * inv3
+        bound = [1e-14 * np.abs(ref[0]), 1e-13 * np.abs(ref[1]), 1e-13 * np.abs(ref[2]),
+                 4e-15 * cond * k4_scale]
         for i in range(4):
             nz = ref[i] != 0.0
             assert np.all(k[i][~nz] == 0.0)  # identity medium / kappa=0: exact zeros
-            err = np.abs(k[i][nz] - ref[i][nz]) / np.abs(ref[i][nz])
-            assert np.all(err <= bound[i][nz]), (tag, i, err.max())
+            err = np.abs(k[i] - ref[i])
+            assert np.all(err[nz] <= bound[i][nz]), (tag, i, (err[nz] / bound[i][nz]).max())
 
 
 @pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2"])
