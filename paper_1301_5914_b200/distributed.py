@@ -1,0 +1,71 @@
+"""Row-split plumbing for one-process-per-GPU runs.
+
+The reference splits target rows into contiguous ranges
+(``partition_targets``, solver.py:405-418), computes each range in a worker
+and concatenates the two half-vectors (solver.py:447-459).  Here every rank
+owns one range on its GPU; after the sweep each rank's rows sit in a
+``[2][m]`` send slot (m = ceil(n / nranks)), one ``ncclAllGather`` fills the
+rank-major ``[nranks][2][m]`` receive buffer, and a permutation kernel
+rebuilds ``out[0:n] ++ out[n:2n]``.  This module is the host-side statement of
+that layout (the CUDA permutation kernel in csrc/hobi_sweep.cu implements the
+same index map) plus the NCCL unique-id exchange over torch.distributed.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+
+def row_range(n: int, nranks: int, rank: int) -> tuple[int, int]:
+    """partition_targets(n, nranks)[rank] (solver.py:405-418)."""
+    base, extra = divmod(n, nranks)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def slot_size(n: int, nranks: int) -> int:
+    return -(-n // nranks)
+
+
+def owner_of(v: np.ndarray, n: int, nranks: int) -> np.ndarray:
+    """Rank owning row v -- the closed form used by permute_kernel."""
+    base, extra = divmod(n, nranks)
+    cut = extra * (base + 1)
+    v = np.asarray(v, dtype=np.int64)
+    return np.where(v < cut, v // (base + 1), extra + (v - cut) // max(base, 1))
+
+
+def pack_rows(phi_rows: np.ndarray, dphi_rows: np.ndarray, m: int) -> np.ndarray:
+    """This rank's send slot [2][m] (tail padded with zeros)."""
+    slot = np.zeros((2, m))
+    slot[0, : phi_rows.size] = phi_rows
+    slot[1, : dphi_rows.size] = dphi_rows
+    return slot
+
+
+def unpack_gathered(recv: np.ndarray, n: int, nranks: int) -> np.ndarray:
+    """[nranks][2][m] gathered slots -> (phi rows ++ dphi rows), length 2n."""
+    recv = np.asarray(recv).reshape(nranks, 2, -1)
+    v = np.arange(n)
+    r = owner_of(v, n, nranks)
+    lo = np.array([row_range(n, nranks, k)[0] for k in range(nranks)])[r]
+    return np.concatenate([recv[r, 0, v - lo], recv[r, 1, v - lo]])
+
+
+def init_nccl_comm(handle, rank: int, world: int) -> None:
+    """Create the library's NCCL communicator: rank 0 draws the unique id,
+    torch.distributed broadcasts the 128 bytes, every rank joins."""
+    import torch.distributed as dist
+
+    from . import _native as N
+
+    lib = N.load()
+    uid = (C.c_ubyte * 128)()
+    if rank == 0:
+        N.check(lib.hobi_comm_unique_id(uid))
+    box = [bytes(uid) if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+    N.check(lib.hobi_comm_init(handle, uid, world, rank))

@@ -239,22 +239,13 @@ def discretize(mesh: FlatMesh, params: PhysicalParams, charges: ChargeSystem,
     handle = _Handle(ctx.value)
     rank, world, _ = _world()
     if world > 1:
-        _init_comm(handle.ptr, rank, world)
+        from .distributed import init_nccl_comm
+
+        try:
+            init_nccl_comm(handle.ptr, rank, world)
+        except N.NativeError as exc:
+            _raise(exc.status)
     return DiscretizedProblem(mesh, params, charges, config.scheme, handle, rule, duffy, (rank, world))
-
-
-def _init_comm(ptr, rank, world):
-    """NCCL communicator for the row split; the unique id travels over torch.distributed."""
-    import torch.distributed as dist
-
-    lib = N.load()
-    uid = (C.c_ubyte * 128)()
-    if rank == 0:
-        _raise(lib.hobi_comm_unique_id(uid))
-    box = [bytes(uid) if rank == 0 else None]
-    dist.broadcast_object_list(box, src=0)
-    uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
-    _raise(lib.hobi_comm_init(ptr, uid, world, rank))
 
 
 def _as_vector(problem, u):

@@ -1,0 +1,66 @@
+"""The C-ABI library loads on CPU and exports every symbol include/hobi.h
+declares (no compute calls without a GPU); the product refuses to run
+without a device instead of falling back to the CPU."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_1301_5914_b200 import _native as N
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "hobi.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hobi_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_expected_entry_points():
+    names = _declared()
+    for must in ("hobi_create", "hobi_matvec", "hobi_matvec_device", "hobi_matvec_rows", "hobi_rhs",
+                 "hobi_energy", "hobi_gmres", "hobi_comm_init", "hobi_destroy", "hobi_bench"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+        assert name in N.SIGNATURES, f"{name} has no ctypes signature"
+    assert set(N.SIGNATURES) <= set(_declared())
+    assert lib.hobi_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", N.LIB_PATH],
+                         capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_no_cpu_fallback_without_device():
+    if N.device_count() > 0:
+        pytest.skip("a GPU is present")
+    from paper_1301_5914_b200 import (ChargeSystem, PhysicalParams, SolverConfig, discretize,
+                                      gmres_solve, icosahedral_sphere)
+
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        discretize(icosahedral_sphere(1), PhysicalParams(1, 80, 0.1), ChargeSystem(np.zeros((0, 3)), []),
+                   SolverConfig())
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        gmres_solve(lambda v: v, np.ones(4), SolverConfig())
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_1301_5914_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "hobi_oracle" not in src and "oracle/" not in src, f
