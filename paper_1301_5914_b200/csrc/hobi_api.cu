@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -532,7 +533,10 @@ int hobi_comm_init(hobi_ctx* c, const unsigned char id[128], int nranks, int ran
   c->comm.nranks = nranks;
   c->comm.rank = rank;
   row_range(c->nt, nranks, rank, &c->lo, &c->hi);
-  if (nranks == 1) return 0;
+  // A single rank needs no collective; HOBI_FORCE_NCCL=1 still builds a
+  // one-rank communicator so the NCCL gather path can be exercised on one GPU.
+  const char* force = getenv("HOBI_FORCE_NCCL");
+  if (nranks == 1 && !(force && force[0] == '1')) return 0;
   auto& a = nccl::api();
   if (!a.loaded) return fail(HOBI_ERR_NCCL, "libnccl.so.2 could not be loaded");
   nccl::UniqueId u;

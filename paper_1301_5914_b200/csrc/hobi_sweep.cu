@@ -460,7 +460,8 @@ int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi,
 
 int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
   int rc;
-  if (c->comm.nranks == 1) return matvec_rows_device(c, u_dev, 0, c->nt, out_dev, out_dev + c->nt);
+  if (c->comm.nranks == 1 && !c->comm.nccl)
+    return matvec_rows_device(c, u_dev, 0, c->nt, out_dev, out_dev + c->nt);
   const int64_t m = c->gather_m;
   if (c->comm.emulated) {  // every rank's rows, computed here, in the gather layout
     for (int r = 0; r < c->comm.nranks; ++r) {

@@ -1,0 +1,42 @@
+"""The NCCL gather path on one GPU: a one-rank communicator (HOBI_FORCE_NCCL=1)
+runs the same send slot -> ncclAllGather -> permutation kernel sequence as an
+8-way split does, and must reproduce the plain operator bitwise."""
+
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def test_single_rank_nccl_gather_path(monkeypatch):
+    pytest.importorskip("torch")
+    import torch  # noqa: F401  (loads libnccl.so.2 into the process, as under torchrun)
+
+    from paper_1301_5914_b200 import (ChargeSystem, FlatMesh, PhysicalParams, SolverConfig,
+                                      discretize, gmres_solve, make_operator, matvec_hobi,
+                                      assemble_rhs)
+    from paper_1301_5914_b200 import _native as N
+
+    g = golden("star_l3")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    params = PhysicalParams(*g["params"])
+    charges = ChargeSystem(g["qpos"], g["q"])
+    plain = discretize(mesh, params, charges, SolverConfig(workers=1))
+    ref = matvec_hobi(plain, g["u"])
+    prob = discretize(mesh, params, charges, SolverConfig(workers=1))
+    lib = N.load()
+    uid = (C.c_ubyte * 128)()
+    N.check(lib.hobi_comm_unique_id(uid))
+    monkeypatch.setenv("HOBI_FORCE_NCCL", "1")
+    N.check(lib.hobi_comm_init(prob.handle, uid, 1, 0))
+    out = matvec_hobi(prob, g["u"])
+    assert np.array_equal(out, ref)
+    cfg = SolverConfig(workers=1, restart=int(g["restart"]))
+    with make_operator(prob, cfg) as op:
+        sol = gmres_solve(op, assemble_rhs(prob), cfg)
+    assert sol.iterations == int(g["iterations"])
