@@ -165,6 +165,12 @@ int hobi_pairs_per_matvec(hobi_ctx* ctx, double* pairs);
 int hobi_bench(hobi_ctx* ctx, const double* u, double* out, int steps, int mode, int flush_l2,
                double* ms);
 
+/* Per-rank cost model of a p-way split on one GPU: `steps` device-timed
+ * applications restricted to rows [lo, hi) (source weights, sweep, Duffy
+ * swap, diagonal -- everything a rank computes before the allgather). */
+int hobi_bench_rows(hobi_ctx* ctx, const double* u, int64_t lo, int64_t hi, int steps, int flush_l2,
+                    double* ms);
+
 /* DFMA throughput probe (FP64 roofline denominator), TFLOP/s over ~`ms` ms. */
 int hobi_probe_fp64_tflops(int device, double ms, double* tflops);
 

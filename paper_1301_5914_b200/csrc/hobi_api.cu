@@ -112,15 +112,13 @@ static int setup_gather(hobi_ctx* c, int nranks) {
 // source-group partition: a function of the problem size only (never of the
 // row split), chosen so an 8-way split still fills 148 SMs several times.
 
-static void choose_groups(hobi_ctx* c) {
+static int choose_groups(hobi_ctx* c) {
   c->n_src_tiles = (int)(c->ns_pad / kSrcTile);
-  const int64_t rows8 = (c->nt + 7) / 8;
-  const int64_t tiles8 = std::max<int64_t>(1, (rows8 + kTargetTile - 1) / kTargetTile);
-  const int64_t want = (1184 + tiles8 - 1) / tiles8;  // 148 SMs x 8 CTAs at 8 GPUs
-  const int64_t maxg = std::max<int64_t>(1, c->n_src_tiles / 4);
-  const int64_t g = std::max<int64_t>(1, std::min(want, maxg));
-  c->tiles_per_group = (int)((c->n_src_tiles + g - 1) / g);
-  c->n_groups = (c->n_src_tiles + c->tiles_per_group - 1) / c->tiles_per_group;
+  std::vector<int2> g = make_groups(c->n_src_tiles, std::max<int64_t>(1, ((c->nt + 7) / 8 + 767) / 768));
+  c->n_groups = (int)g.size();
+  if (c->groups.alloc(g.size())) return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemcpy(c->groups.p, g.data(), g.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  return 0;
 }
 
 static int common_init(hobi_ctx* c, int device, double eps1, double eps2, double kappa) {
@@ -151,9 +149,11 @@ static int common_init(hobi_ctx* c, int device, double eps1, double eps2, double
 static int alloc_operands(hobi_ctx* c) {
   c->nt_pad = ((c->nt + kTargetTile - 1) / kTargetTile) * kTargetTile;
   c->ns_pad = std::max<int64_t>(kSrcTile, ((c->ns + kSrcTile - 1) / kSrcTile) * kSrcTile);
-  choose_groups(c);
+  int rcg = choose_groups(c);
+  if (rcg) return rcg;
   if (c->tgt.alloc(6 * c->nt_pad) || c->src.alloc(c->ns_pad * kSrcStride) ||
-      c->part.alloc((size_t)c->n_groups * 2 * c->nt_pad) || c->u.alloc(std::max<int64_t>(1, 2 * c->nt)) ||
+      c->part.alloc((size_t)c->n_groups * 2 * c->nt_pad) || c->ticket.alloc(1) ||
+      c->u.alloc(std::max<int64_t>(1, 2 * c->nt)) ||
       c->out.alloc(std::max<int64_t>(1, 2 * c->nt)))
     return HOBI_ERR_CUDA;
   c->lo = 0;
@@ -626,6 +626,35 @@ int hobi_sweep_variant(hobi_ctx* c, int variant, int* count, char* name, int nam
     snprintf(name, name_len, "%s", sweep_variant_name(c->sweep_variant));
   }
   return 0;
+}
+
+int hobi_bench_rows(hobi_ctx* c, const double* u, int64_t lo, int64_t hi, int steps, int flush_l2,
+                    double* ms) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (lo < 0 || hi > c->nt || lo > hi || steps < 0) return fail(HOBI_ERR_VALUE, "bad bench_rows arguments");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  DevBuf<unsigned char> scratch;
+  const size_t flush_bytes = (size_t)512 << 20;
+  if (flush_l2 && scratch.alloc(flush_bytes)) return HOBI_ERR_CUDA;
+  cudaEvent_t e0, e1;
+  HOBI_CUDA(cudaEventCreate(&e0));
+  HOBI_CUDA(cudaEventCreate(&e1));
+  HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, 2 * c->nt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int rc = 0;
+  for (int i = 0; i < steps && !rc; ++i) {
+    if (flush_l2) HOBI_CUDA(cudaMemsetAsync(scratch.p, i & 0xff, flush_bytes, c->stream));
+    HOBI_CUDA(cudaEventRecord(e0, c->stream));
+    rc = matvec_rows_device(c, c->u.p, lo, hi, c->out.p, c->out.p + (hi - lo));
+    if (rc) break;
+    HOBI_CUDA(cudaEventRecord(e1, c->stream));
+    HOBI_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    HOBI_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    ms[i] = t;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return rc;
 }
 
 int hobi_pairs_per_matvec(hobi_ctx* c, double* pairs) {

@@ -89,7 +89,8 @@ struct hobi_ctx {
   int64_t ns = 0;          // regular sources (nf*nq for hobi, nf for lobi)
   int nq = 0, nd = 0;
   int64_t ns_pad = 0, nt_pad = 0;
-  int n_src_tiles = 0, tiles_per_group = 0, n_groups = 0;
+  int n_src_tiles = 0, n_groups = 0;
+  hobi::DevBuf<int2> groups;                 // source groups: (first tile, tile count)
   int64_t lo = 0, hi = 0;  // owned rows
 
   // geometry (physical units)
@@ -105,6 +106,7 @@ struct hobi_ctx {
   hobi::DevBuf<double> tgt;                  // (6, nt_pad) scaled SoA
   hobi::DevBuf<double> src;                  // (ns_pad, 12) scaled AoS records
   hobi::DevBuf<double> part;                 // (n_groups, 2, nt_pad)
+  hobi::DevBuf<unsigned> ticket;             // work-item counter of the persistent sweep
   hobi::DevBuf<double> corr;                 // (3nf, 2) Duffy-minus-regular per pair
   hobi::DevBuf<double> u, out;               // (2nt)
   hobi::DevBuf<double> gather_send, gather_recv;  // (2*m), (nranks*2*m)
@@ -119,7 +121,7 @@ struct hobi_ctx {
   int64_t sweep_launches = 0;
   int64_t launches = 0;
   bool timing = true;
-  int sweep_variant = 4;  // index into the sweep tuning table (hobi_sweep.cu): R4_minb3_unroll1
+  int sweep_variant = 7;  // index into the sweep tuning table (hobi_sweep.cu): R6_minb2_unroll1
 };
 
 namespace hobi {
@@ -132,6 +134,7 @@ int build_geometry(hobi_ctx* c, const int* pair_of_slot, int* first_bad_slot, in
 // sweep (hobi_sweep.cu)
 int upload_exp_table();
 int collect_sweep_timing(hobi_ctx* c);
+std::vector<int2> make_groups(int n_src_tiles, int64_t target_tiles_at_8);
 int sweep_variant_count();
 const char* sweep_variant_name(int v);
 int prepare_targets(hobi_ctx* c);

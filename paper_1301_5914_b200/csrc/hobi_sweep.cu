@@ -15,6 +15,7 @@
 // (cp.async.bulk + mbarrier).  Source groups depend only on the problem, never
 // on the row split, so every row's sum is bitwise identical for any number of
 // GPUs (solver.py:12-17).
+#include <algorithm>
 #include <cmath>
 
 #include "hobi_fastmath.cuh"
@@ -72,104 +73,129 @@ constexpr uint32_t kTileBytes = kSrcTile * kSrcStride * sizeof(double);
 constexpr size_t kSweepSmem =
     (size_t)kStages * kTileBytes + kExpTable * sizeof(double) + kStages * sizeof(uint64_t);
 
+// Persistent, dynamically scheduled sweep.  Work item = (target tile, source
+// group); items are numbered group-major so CTAs running concurrently share a
+// source group in L2, and handed out by an atomic ticket so every SM stays busy
+// to the end of the launch at any row split (no wave quantisation).  Each
+// item's result depends only on its (tile, group), never on which CTA ran it,
+// so the sums stay deterministic.  Source tiles of every item flow through one
+// continuous kStages-deep TMA ring: `seq` counts tiles across items.
 template <int MODE, bool FULL, bool SELF, int R, int MINB, int UNROLL>
 __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
     const double* __restrict__ tgt, int64_t ldt, int64_t t_begin, int64_t t_end,
-    const double* __restrict__ src, int n_src_tiles, int tiles_per_group, double* __restrict__ part,
-    int64_t ldp) {
+    const double* __restrict__ src, const int2* __restrict__ groups, int n_groups,
+    double* __restrict__ part, int64_t ldp, unsigned* __restrict__ ticket) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
   double* etab = ring + kStages * kSrcTile * kSrcStride;
   uint64_t* bars = reinterpret_cast<uint64_t*>(etab + kExpTable);
+  __shared__ int item_sh;
 
-  const int g = blockIdx.y;
-  const int tile0 = g * tiles_per_group;
-  const int ntl = min(tiles_per_group, n_src_tiles - tile0);
-  const int64_t tb = t_begin + (int64_t)blockIdx.x * (kSweepThreads * R) + threadIdx.x;
+  constexpr int kTile = kSweepThreads * R;
+  const int n_ttiles = (int)((t_end - t_begin + kTile - 1) / kTile);
+  const int n_items = n_ttiles * n_groups;
 
-  double tx[R], ty[R], tz[R], nx[R], ny[R], nz[R];
-  double a1[R], a2[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    int64_t t = min(tb + q * kSweepThreads, t_end - 1);  // padded threads recompute the last row
-    tx[q] = tgt[t];
-    ty[q] = tgt[ldt + t];
-    tz[q] = tgt[2 * ldt + t];
-    nx[q] = tgt[3 * ldt + t];
-    ny[q] = tgt[4 * ldt + t];
-    nz[q] = tgt[5 * ldt + t];
-    a1[q] = 0.0;
-    a2[q] = 0.0;
-  }
   if (MODE == kScreened)
     for (int i = threadIdx.x; i < kExpTable; i += kSweepThreads) etab[i] = g_exp_table[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  const double* gsrc = src + (int64_t)tile0 * kSrcTile * kSrcStride;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages - 1 && s < ntl; ++s) {
-      mbar_expect_tx(&bars[s], kTileBytes);
-      bulk_g2s(ring + s * kSrcTile * kSrcStride, gsrc + (int64_t)s * kSrcTile * kSrcStride,
-               kTileBytes, &bars[s]);
-    }
-  }
-  for (int it = 0; it < ntl; ++it) {
-    if (threadIdx.x == 0 && it + kStages - 1 < ntl) {
-      const int nxt = it + kStages - 1;
-      const int s = nxt % kStages;
+  uint32_t seq = 0;  // source tiles consumed so far by this CTA (ring position)
+  for (;;) {
+    if (threadIdx.x == 0) item_sh = (int)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int item = item_sh;
+    __syncthreads();
+    if (item >= n_items) break;
+    const int g = item / n_ttiles;
+    const int tt = item - g * n_ttiles;
+    const int2 grp = groups[g];  // (first source tile, tile count)
+    const int tile0 = grp.x;
+    const int ntl = grp.y;
+    // thread owns R consecutive targets; warps entirely past the end skip the math
+    const int64_t tb = t_begin + (int64_t)tt * kTile + (int64_t)threadIdx.x * R;
+    const bool warp_live = t_begin + (int64_t)tt * kTile + (int64_t)(threadIdx.x & ~31) * R < t_end;
+    const double* gsrc = src + (int64_t)tile0 * kSrcTile * kSrcStride;
+    if (threadIdx.x == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bars[s], kTileBytes);
-      bulk_g2s(ring + s * kSrcTile * kSrcStride, gsrc + (int64_t)nxt * kSrcTile * kSrcStride,
-               kTileBytes, &bars[s]);
-    }
-    const int s = it % kStages;
-    mbar_wait(&bars[s], (uint32_t)((it / kStages) & 1));
-    const double2* rec = reinterpret_cast<const double2*>(ring + s * kSrcTile * kSrcStride);
-#pragma unroll UNROLL
-    for (int j = 0; j < kSrcTile; ++j) {
-      const double2 p01 = rec[6 * j + 0], p2m0 = rec[6 * j + 1], m12 = rec[6 * j + 2];
-      double2 w01 = rec[6 * j + 3], w23 = rec[6 * j + 4], w45 = rec[6 * j + 5];
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        double sx = p01.x, sy = p01.y, sz = p2m0.x;
-        if (SELF) {
-          // LOBI self pair: displacement forced to (1,0,0) and weights to 0, so
-          // it contributes exactly +0 (solver.py:303-310).
-          const bool self = ((int64_t)(tile0 + it) * kSrcTile + j) == tb + q * kSweepThreads;
-          if (self) {
-            sx = tx[q] - 1.0;
-            sy = ty[q];
-            sz = tz[q];
-            w01 = make_double2(0.0, 0.0);
-            w23 = w01;
-            w45 = w01;
-          }
-        }
-        if (MODE == kScreened)
-          pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz,
-                              p2m0.y, m12.x, m12.y, w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, etab,
-                              a1[q], a2[q]);
-        else
-          pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz,
-                             p2m0.y, m12.x, m12.y, w23.x, w45.x, a1[q], a2[q]);
-        if (SELF) {
-          w01 = rec[6 * j + 3];
-          w23 = rec[6 * j + 4];
-          w45 = rec[6 * j + 5];
-        }
+      for (int s = 0; s < kStages - 1 && s < ntl; ++s) {
+        const int st = (int)((seq + s) % kStages);
+        mbar_expect_tx(&bars[st], kTileBytes);
+        bulk_g2s(ring + st * kSrcTile * kSrcStride, gsrc + (int64_t)s * kSrcTile * kSrcStride,
+                 kTileBytes, &bars[st]);
       }
     }
-    __syncthreads();
-  }
+    double tx[R], ty[R], tz[R], nx[R], ny[R], nz[R];
+    double a1[R], a2[R];
 #pragma unroll
-  for (int q = 0; q < R; ++q) {
-    int64_t t = tb + q * kSweepThreads;
-    if (t < t_end) {
-      part[(2 * (int64_t)g) * ldp + t] = a1[q];
-      if (FULL) part[(2 * (int64_t)g + 1) * ldp + t] = a2[q];
+    for (int q = 0; q < R; ++q) {
+      int64_t t = min(tb + q, t_end - 1);  // padded slots recompute the last row
+      tx[q] = tgt[t];
+      ty[q] = tgt[ldt + t];
+      tz[q] = tgt[2 * ldt + t];
+      nx[q] = tgt[3 * ldt + t];
+      ny[q] = tgt[4 * ldt + t];
+      nz[q] = tgt[5 * ldt + t];
+      a1[q] = 0.0;
+      a2[q] = 0.0;
+    }
+    for (int it = 0; it < ntl; ++it) {
+      if (threadIdx.x == 0 && it + kStages - 1 < ntl) {
+        const int nxt = it + kStages - 1;
+        const int st = (int)((seq + nxt) % kStages);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bars[st], kTileBytes);
+        bulk_g2s(ring + st * kSrcTile * kSrcStride, gsrc + (int64_t)nxt * kSrcTile * kSrcStride,
+                 kTileBytes, &bars[st]);
+      }
+      const uint32_t pos = seq + it;
+      const int st = (int)(pos % kStages);
+      mbar_wait(&bars[st], (pos / kStages) & 1u);
+      const double2* rec = reinterpret_cast<const double2*>(ring + st * kSrcTile * kSrcStride);
+#pragma unroll UNROLL
+      for (int j = 0; j < (warp_live ? kSrcTile : 0); ++j) {
+        const double2 p01 = rec[6 * j + 0], p2m0 = rec[6 * j + 1], m12 = rec[6 * j + 2];
+        double2 w01 = rec[6 * j + 3], w23 = rec[6 * j + 4], w45 = rec[6 * j + 5];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          double sx = p01.x, sy = p01.y, sz = p2m0.x;
+          if (SELF) {
+            // LOBI self pair: displacement forced to (1,0,0) and weights to 0, so
+            // it contributes exactly +0 (solver.py:303-310).
+            const bool self = ((int64_t)(tile0 + it) * kSrcTile + j) == tb + q;
+            if (self) {
+              sx = tx[q] - 1.0;
+              sy = ty[q];
+              sz = tz[q];
+              w01 = make_double2(0.0, 0.0);
+              w23 = w01;
+              w45 = w01;
+            }
+          }
+          if (MODE == kScreened)
+            pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, p2m0.y, m12.x,
+                                m12.y, w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, etab, a1[q], a2[q]);
+          else
+            pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, p2m0.y, m12.x,
+                               m12.y, w23.x, w45.x, a1[q], a2[q]);
+          if (SELF) {
+            w01 = rec[6 * j + 3];
+            w23 = rec[6 * j + 4];
+            w45 = rec[6 * j + 5];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    seq += (uint32_t)ntl;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      int64_t t = tb + q;
+      if (t < t_end) {
+        part[(2 * (int64_t)g) * ldp + t] = a1[q];
+        if (FULL) part[(2 * (int64_t)g + 1) * ldp + t] = a2[q];
+      }
     }
   }
 }
@@ -319,8 +345,8 @@ int collect_sweep_timing(hobi_ctx* c) {
 
 namespace {
 
-typedef void (*SweepFn)(const double*, int64_t, int64_t, int64_t, const double*, int, int, double*,
-                        int64_t);
+typedef void (*SweepFn)(const double*, int64_t, int64_t, int64_t, const double*, const int2*, int,
+                        double*, int64_t, unsigned*);
 
 struct SweepVariant {
   SweepFn fn;
@@ -333,14 +359,15 @@ struct SweepVariant {
 #define HOBI_V(R, M, U) \
   { sweep_kernel<kScreened, true, false, R, M, U>, R, "R" #R "_minb" #M "_unroll" #U }
 static const SweepVariant kVariants[] = {
-    HOBI_V(2, 1, 2), HOBI_V(2, 6, 2), HOBI_V(2, 8, 2), HOBI_V(1, 8, 2), HOBI_V(4, 3, 1),
-    HOBI_V(4, 4, 1), HOBI_V(3, 4, 1), HOBI_V(2, 1, 1), HOBI_V(2, 6, 1), HOBI_V(1, 8, 4),
+    HOBI_V(2, 1, 2), HOBI_V(2, 6, 2), HOBI_V(4, 3, 2), HOBI_V(1, 8, 2), HOBI_V(4, 3, 1),
+    HOBI_V(4, 4, 1), HOBI_V(3, 4, 1), HOBI_V(6, 2, 1), HOBI_V(8, 2, 1), HOBI_V(3, 4, 2),
+    HOBI_V(4, 4, 2), HOBI_V(5, 3, 1),
 };
 #undef HOBI_V
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_t t1, bool full,
-                 double* part, int64_t ldp, int n_groups, int tiles_per_group) {
+                 double* part, int64_t ldp, const int2* groups, int n_groups) {
   if (t1 <= t0) return 0;
   const bool self = c->scheme == kLobi && full;
   SweepFn fn;
@@ -360,7 +387,12 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
                       : sweep_kernel<kLaplace, false, false, kSweepR, 1, 2>);
   }
   HOBI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
-  dim3 grid(nblk(t1 - t0, kSweepThreads * r), n_groups);
+  int per_sm = 0, sms = 0;
+  HOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSweepThreads, kSweepSmem));
+  HOBI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * r) * n_groups;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)std::max(per_sm, 1) * sms));
+  HOBI_CUDA(cudaMemsetAsync(c->ticket.p, 0, sizeof(unsigned), c->stream));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {  // brackets are read lazily by collect_sweep_timing: no sync here
     if (c->ev_used + 2 > c->ev_pool.size()) {
@@ -375,8 +407,8 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
     c->ev_used += 2;
     HOBI_CUDA(cudaEventRecord(e0, c->stream));
   }
-  fn<<<grid, kSweepThreads, kSweepSmem, c->stream>>>(tgt, ldt, t0, t1, c->src.p, c->n_src_tiles,
-                                                     tiles_per_group, part, ldp);
+  fn<<<grid, kSweepThreads, kSweepSmem, c->stream>>>(tgt, ldt, t0, t1, c->src.p, groups, n_groups,
+                                                     part, ldp, c->ticket.p);
   HOBI_CUDA(cudaGetLastError());
   c->launches++;
   if (c->timing) {
@@ -400,6 +432,40 @@ void weight_constants(const Physics& p, double* kA, double* kB, double* kC, doub
 }
 
 }  // namespace
+
+// Fixed partition of the source tiles into groups -- a function of the
+// problem size only, so row sums never depend on the row split.  Bulk groups
+// of B tiles come first; the end of the source axis is cut into groups that
+// halve in size (B/2, B/2, B/4, B/4, ..., 1, 1), so the group-major work queue
+// of the persistent sweep ends with small items and the dynamic tail is short.
+// B gives an 8-way split with `tiles8` target tiles per rank ~16 work items
+// per resident CTA slot (2 per SM x 148 SMs).
+std::vector<int2> make_groups(int n_src_tiles, int64_t tiles8) {
+  std::vector<int2> g;
+  if (n_src_tiles <= 0) return g;
+  const int64_t want = std::max<int64_t>(1, (16 * 2 * 148 + tiles8 - 1) / tiles8);
+  const int B = (int)std::max<int64_t>(1, (n_src_tiles + want - 1) / want);
+  std::vector<int> tail;
+  int tail_sum = 0;
+  for (int s = 1; s < B; s *= 2) {
+    if (tail_sum + 2 * s > n_src_tiles / 2) break;
+    tail.push_back(s);
+    tail.push_back(s);
+    tail_sum += 2 * s;
+  }
+  int t = 0;
+  const int bulk = n_src_tiles - tail_sum;
+  for (; t + B <= bulk; t += B) g.push_back(make_int2(t, B));
+  if (t < bulk) {
+    g.push_back(make_int2(t, bulk - t));
+    t = bulk;
+  }
+  for (int k = (int)tail.size() - 1; k >= 0; --k) {
+    g.push_back(make_int2(t, tail[k]));
+    t += tail[k];
+  }
+  return g;
+}
 
 int sweep_variant_count() { return kNumVariants; }
 const char* sweep_variant_name(int v) { return (v >= 0 && v < kNumVariants) ? kVariants[v].name : ""; }
@@ -440,8 +506,8 @@ int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi,
   if (hi <= lo) return 0;
   int rc;
   if ((rc = update_weights(c, u_dev))) return rc;
-  if ((rc = launch_sweep(c, c->tgt.p, c->nt_pad, lo, hi, true, c->part.p, c->nt_pad, c->n_groups,
-                         c->tiles_per_group)))
+  if ((rc = launch_sweep(c, c->tgt.p, c->nt_pad, lo, hi, true, c->part.p, c->nt_pad, c->groups.p,
+                         c->n_groups)))
     return rc;
   const double* corr = nullptr;
   const int* starts = nullptr;
@@ -492,9 +558,11 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, 
   const int64_t ldc = ((nc + kTargetTile - 1) / kTargetTile) * kTargetTile;
   DevBuf<double> dq, dqpos, tq, part, e;
   if (dq.alloc(nc) || dqpos.alloc(3 * nc) || tq.alloc(6 * ldc) || e.alloc(1)) return HOBI_ERR_CUDA;
-  int tiles = c->n_src_tiles;
-  int tiles_per_group = std::max(4, (int)((tiles + 15) / 16));
-  int groups = (tiles + tiles_per_group - 1) / tiles_per_group;
+  std::vector<int2> gtab = make_groups(c->n_src_tiles, std::max<int64_t>(1, (nc + 767) / 768));
+  const int groups = (int)gtab.size();
+  DevBuf<int2> dgroups;
+  if (dgroups.alloc(groups)) return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemcpyAsync(dgroups.p, gtab.data(), groups * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
   if (part.alloc((size_t)groups * 2 * ldc)) return HOBI_ERR_CUDA;
   HOBI_CUDA(cudaMemcpyAsync(dq.p, q, nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   HOBI_CUDA(cudaMemcpyAsync(dqpos.p, qpos, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -505,7 +573,7 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, 
   if ((rc = update_weights(c, x_dev))) return rc;
   bool timing = c->timing;
   c->timing = false;
-  rc = launch_sweep(c, tq.p, ldc, 0, nc, false, part.p, ldc, groups, tiles_per_group);
+  rc = launch_sweep(c, tq.p, ldc, 0, nc, false, part.p, ldc, dgroups.p, groups);
   c->timing = timing;
   if (rc) return rc;
   energy_reduce_kernel<<<1, 32, 0, c->stream>>>(part.p, ldc, groups, dq.p, nc, e.p);
