@@ -7,6 +7,10 @@
 // triangular solve stay on the host in the reference's exact scalar order.
 #include <cooperative_groups.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cmath>
 #include <limits>
 #include <vector>
@@ -175,6 +179,10 @@ int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
   HOBI_CUDA(cudaMemsetAsync(ws.x.p, 0, n * sizeof(double), stream));
   int total = 0;
   double best = std::numeric_limits<double>::infinity();
+  const bool trace = getenv("HOBI_GMRES_TRACE") && getenv("HOBI_GMRES_TRACE")[0] == '1';
+  auto now = [] { return std::chrono::duration<double, std::milli>(
+                      std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double t_mv = 0.0, t_orth = 0.0;
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hcol(m + 2), y(m);
   auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * m + j]; };
   while (true) {
@@ -213,8 +221,10 @@ int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
     g[0] = beta;
     int j = 0;
     while (j < m && total < max_it) {
+      double ta = trace ? (cudaStreamSynchronize(stream), now()) : 0.0;
       if ((rc = op->apply(ws.V.p + (int64_t)j * ws.ldv, ws.w.p))) return rc;
       ++*matvecs;
+      double tb = trace ? (cudaStreamSynchronize(stream), now()) : 0.0;
       {
         double* Vp = ws.V.p;
         int64_t ldv = ws.ldv, nn = n;
@@ -228,6 +238,12 @@ int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
       HOBI_CUDA(cudaMemcpyAsync(hcol.data(), ws.hcol.p, (j + 2) * sizeof(double),
                                 cudaMemcpyDeviceToHost, stream));
       HOBI_CUDA(cudaStreamSynchronize(stream));
+      if (trace) {
+        double tc = now();
+        t_mv += tb - ta;
+        t_orth += tc - tb;
+        fprintf(stderr, "gmres it %d j %d matvec %.3f ms orth+sync %.3f ms\n", total, j, tb - ta, tc - tb);
+      }
       for (int i = 0; i <= j + 1; ++i) Hat(i, j) = hcol[i];
       for (int i = 0; i < j; ++i) {  // apply previous rotations (solver.py:544-547)
         double tmp = cs[i] * Hat(i, j) + sn[i] * Hat(i + 1, j);

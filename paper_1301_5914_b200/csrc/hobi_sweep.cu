@@ -314,17 +314,28 @@ __global__ void permute_kernel(const double* __restrict__ recv, int64_t m, int64
   out[nt + v] = recv[(r * 2 + 1) * m + (v - lo)];
 }
 
-__global__ void energy_reduce_kernel(const double* __restrict__ part, int64_t ldp, int n_groups,
-                                     const double* __restrict__ q, int64_t nc, double* __restrict__ out) {
-  // one thread, fixed order: total += q_k * sum_k (solver.py:608-614)
-  if (blockIdx.x || threadIdx.x) return;
-  double total = 0.0;
-  for (int64_t k = 0; k < nc; ++k) {
-    double s = part[k];
-    for (int g = 1; g < n_groups; ++g) s += part[(2 * (int64_t)g) * ldp + k];
-    total += q[k] * s;
+// Energy (solver.py:608-614): per-charge group sums in fixed group order,
+// q_k * sum_k, then one block folds the charges in a fixed tree order.
+__global__ void energy_charge_kernel(const double* __restrict__ part, int64_t ldp, int n_groups,
+                                     const double* __restrict__ q, int64_t nc, double* __restrict__ v) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nc) return;
+  double s = part[k];
+  for (int g = 1; g < n_groups; ++g) s += part[(2 * (int64_t)g) * ldp + k];
+  v[k] = q[k] * s;
+}
+
+__global__ void energy_fold_kernel(const double* __restrict__ v, int64_t nc, double* __restrict__ out) {
+  __shared__ double sh[1024];
+  double acc = 0.0;
+  for (int64_t k = threadIdx.x; k < nc; k += blockDim.x) acc += v[k];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
   }
-  out[0] = 0.5 * kFourPi * kKcal * total;
+  if (threadIdx.x == 0) out[0] = 0.5 * kFourPi * kKcal * sh[0];
 }
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -576,8 +587,11 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, 
   rc = launch_sweep(c, tq.p, ldc, 0, nc, false, part.p, ldc, dgroups.p, groups);
   c->timing = timing;
   if (rc) return rc;
-  energy_reduce_kernel<<<1, 32, 0, c->stream>>>(part.p, ldc, groups, dq.p, nc, e.p);
-  c->launches++;
+  DevBuf<double> v;
+  if (v.alloc(nc)) return HOBI_ERR_CUDA;
+  energy_charge_kernel<<<nblk(nc, 256), 256, 0, c->stream>>>(part.p, ldc, groups, dq.p, nc, v.p);
+  energy_fold_kernel<<<1, 1024, 0, c->stream>>>(v.p, nc, e.p);
+  c->launches += 2;
   HOBI_CUDA(cudaGetLastError());
   HOBI_CUDA(cudaMemcpyAsync(energy, e.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
