@@ -5,7 +5,8 @@ GMRES, energy, NCCL row split), behind the reference package's Python API
 C ABI: ``include/hobi.h``.
 """
 
-from .mesh import ChargeSystem, FlatMesh, MeshFormatError, MeshValidationError, icosahedral_sphere
+from .mesh import (ChargeSystem, FlatMesh, MeshFormatError, MeshValidationError, flat_area,
+                   icosahedral_sphere, parse_charges, parse_msms, radial_project, write_msms)
 from .physics import FOUR_PI, KCAL_MOL_PER_E2_ANG, PhysicalParams, SingularityError
 from .quadrature import TriangleRule, duffy_rule, gauss_radau_rule
 from .solver import (
@@ -38,4 +39,5 @@ __all__ = [
     "TriangleRule", "apply_rows", "assemble_rhs", "convergence_order", "discretize", "duffy_rule",
     "gauss_radau_rule", "gmres_solve", "icosahedral_sphere", "make_operator", "matvec_hobi",
     "matvec_lobi", "partition_targets", "solvation_energy", "solve", "surface_potential_error",
+    "flat_area", "parse_charges", "parse_msms", "radial_project", "write_msms",
 ]

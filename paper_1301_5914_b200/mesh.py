@@ -189,3 +189,108 @@ def icosahedral_sphere(level: int, radius: float = 1.0, center=(0.0, 0.0, 0.0)) 
     v, f = unit_icosphere(level)
     c = np.asarray(center, dtype=float)
     return FlatMesh(vertices=c + radius * v, normals=v.copy(), faces=f)
+
+
+# ----------------------------------------------------------------------------
+# MSMS .vert/.face text and charge files (pbbem/mesh.py:113-227), SURVEY.md 8(f) f2
+
+
+def _records(text: str):
+    """(1-based line number, tokens) of every non-blank line, '#' comments removed."""
+    for number, raw in enumerate(text.splitlines(), start=1):
+        body = raw.split("#", 1)[0].split()
+        if body:
+            yield number, body
+
+
+def _parses(tok: str, kind) -> bool:
+    try:
+        kind(tok)
+        return True
+    except ValueError:
+        return False
+
+
+def parse_msms(vert_text: str, face_text: str) -> FlatMesh:
+    """MSMS .vert/.face contents -> validated FlatMesh (pbbem/mesh.py:141-185).
+
+    Records are recognised by shape, headers skipped: a vertex record starts
+    with a real and has >= 6 fields (x y z nx ny nz), a face record has >= 3
+    leading integers (1-based).  A record that breaks midway is an error with
+    its line number; normals are renormalised (MSMS prints 3 digits).
+    """
+    rows = []
+    for number, tok in _records(vert_text):
+        if len(tok) < 6 or not _parses(tok[0], float):
+            continue
+        try:
+            rows.append([float(t) for t in tok[:6]])
+        except ValueError as exc:
+            raise MeshFormatError(f".vert line {number}: {exc}") from None
+    tris = []
+    for number, tok in _records(face_text):
+        if len(tok) < 3 or not all(_parses(t, int) for t in tok[:3]):
+            continue
+        ijk = tuple(int(t) for t in tok[:3])
+        if min(ijk) < 1:
+            raise MeshFormatError(f".face line {number}: vertex indices are 1-based, got {ijk}")
+        tris.append(tuple(i - 1 for i in ijk))
+    if not rows:
+        raise MeshFormatError("no vertex records found in .vert text")
+    if not tris:
+        raise MeshFormatError("no face records found in .face text")
+    data = np.asarray(rows, dtype=float)
+    nrm = data[:, 3:6]
+    length = np.linalg.norm(nrm, axis=1)
+    zero = np.flatnonzero(length < 1e-300)
+    if zero.size:
+        raise MeshFormatError(f"vertex {zero[0]} has a zero normal")
+    mesh = FlatMesh(vertices=data[:, :3], normals=nrm / length[:, None],
+                    faces=np.asarray(tris, dtype=np.int64))
+    mesh.validate()
+    return mesh
+
+
+def write_msms(mesh: FlatMesh) -> tuple[str, str]:
+    """Render a mesh as MSMS-style (vert_text, face_text) that parse_msms reads back
+    exactly: full-precision reprs, comment headers (pbbem/mesh.py:188-207)."""
+    vert = ["# vertices: x y z nx ny nz", f"{mesh.n_vertices} 1 1.0 1.0"]
+    for p, n in zip(mesh.vertices.tolist(), mesh.normals.tolist()):
+        vert.append(" ".join(repr(float(c)) for c in (*p, *n)) + " 0 0 0")
+    face = ["# faces: i j k (1-based)", f"{mesh.n_faces} 1"]
+    face.extend(f"{a + 1} {b + 1} {c + 1} 1 1" for a, b, c in mesh.faces.tolist())
+    return "\n".join(vert) + "\n", "\n".join(face) + "\n"
+
+
+def parse_charges(text: str) -> ChargeSystem:
+    """'x y z q' records (a 5th radius column is ignored) -> ChargeSystem (pbbem/mesh.py:210-227)."""
+    rows = []
+    for number, tok in _records(text):
+        if len(tok) < 4:
+            raise MeshFormatError(f"charge line {number}: need at least 'x y z q', got {tok!r}")
+        try:
+            rows.append([float(t) for t in tok[:4]])
+        except ValueError as exc:
+            raise MeshFormatError(f"charge line {number}: {exc}") from None
+    data = np.asarray(rows, dtype=float).reshape(-1, 4)
+    return ChargeSystem(positions=data[:, :3], charges=data[:, 3])
+
+
+def radial_project(mesh: FlatMesh, center, radius: float) -> FlatMesh:
+    """Snap every vertex onto |x - center| = radius with radial normals (pbbem/mesh.py:303-321)."""
+    if radius <= 0.0:
+        raise ValueError(f"radius must be positive, got {radius}")
+    c = np.asarray(center, dtype=float)
+    d = mesh.vertices - c
+    length = np.linalg.norm(d, axis=1)
+    zero = np.flatnonzero(length < 1e-300)
+    if zero.size:
+        raise ValueError(f"vertex {zero[0]} coincides with the center")
+    n = d / length[:, None]
+    return FlatMesh(vertices=c + radius * n, normals=n, faces=mesh.faces)
+
+
+def flat_area(mesh: FlatMesh) -> float:
+    """Total area of the flat triangles (pbbem/mesh.py:324-328)."""
+    x = mesh.vertices[mesh.faces]
+    return 0.5 * float(np.linalg.norm(np.cross(x[:, 1] - x[:, 0], x[:, 2] - x[:, 0]), axis=1).sum())

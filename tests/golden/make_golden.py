@@ -123,7 +123,48 @@ def degenerate_case():
     print("degenerate:", msg, flush=True)
 
 
+def msms_case():
+    """The reference's MSMS writer/reader and charge parser on a curved mesh plus
+    malformed inputs (mesh.py:141-227): texts, parsed arrays, error messages."""
+    from pbbem import mesh as rm
+
+    star = StarShape.from_seed(16.0, seed=3).surface(2)
+    ref = rm.FlatMesh(vertices=star.vertices, normals=star.normals, faces=star.faces)
+    vert, face = rm.write_msms(ref)
+    # MSMS-style headers, comments, 3-digit normals, extra columns
+    messy_vert = "# MSMS vertices\n#faces #sphere density probe_r\n%d 1 1.50 1.40\n" % star.n_vertices
+    for p, n in zip(star.vertices, star.normals):
+        messy_vert += "%.6f %.6f %.6f %.3f %.3f %.3f 0 %d 2\n" % (*p, *n, 7)
+    messy_face = "# MSMS faces\n%d 1 1.50 1.40\n" % star.n_faces + "".join(
+        "%d %d %d 1 4  # tri\n" % tuple(f + 1) for f in star.faces)
+    parsed = rm.parse_msms(messy_vert, messy_face)
+    errors = []
+    for v, f in (("1.0 0.0 0.0 0.6 0.6 0.6\n2.0 nope 0.0 0.6 0.6 0.6\n", "1 1 1\n"),
+                 ("1.0 0.0 0.0 0.6 0.6 0.6\n" * 3, "0 1 2\n"),
+                 ("1 0 0 0 0 0\n" * 3, "1 2 3\n"), ("# nothing\n", "1 2 3\n"),
+                 ("1.0 0.0 0.0 0.6 0.6 0.6\n", "# none\n")):
+        try:
+            rm.parse_msms(v, f)
+            errors.append("")
+        except Exception as exc:  # noqa: BLE001
+            errors.append(f"{type(exc).__name__}: {exc}")
+    charges_txt = "# x y z q r\n1.5 -2 0.25 0.5 1.8\n\n-1e-3 0 4 -0.25\n  2 2 2 1  # ion\n"
+    ch = rm.parse_charges(charges_txt)
+    np.savez_compressed(os.path.join(HERE, "msms.npz"), vertices=star.vertices, normals=star.normals,
+                        faces=star.faces, vert_text=np.array(vert), face_text=np.array(face),
+                        messy_vert=np.array(messy_vert), messy_face=np.array(messy_face),
+                        parsed_vertices=parsed.vertices, parsed_normals=parsed.normals,
+                        parsed_faces=parsed.faces, errors=np.array(errors),
+                        charges_text=np.array(charges_txt), charges_pos=ch.positions, charges_q=ch.charges)
+    print("msms: done", flush=True)
+
+
 def main():
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        return
+    msms_case()
     kernel_table()
     degenerate_case()
     star = StarShape.from_seed(16.0, seed=3)
