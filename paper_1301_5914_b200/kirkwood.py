@@ -1,0 +1,157 @@
+"""Analytic Kirkwood solutions for charges inside a dielectric sphere.
+
+The validator that follows a solve for configs 1-2,
+restated from the reference (``pbbem/kirkwood.py:59-263``): Laplace
+harmonics inside, modified spherical Bessel functions k_n(kappa r) outside,
+matched by continuity of phi and eps dphi/dr at r = a.  Vectorised over
+charges and evaluation points (the reference loops over charges); host numpy,
+O(N_c * N_points * n_terms).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .mesh import ChargeSystem
+from .physics import FOUR_PI, KCAL_MOL_PER_E2_ANG, PhysicalParams
+
+
+class NotCenteredError(ValueError):
+    """The closed form was asked about an eccentric or multi-charge system."""
+
+
+@dataclass(frozen=True)
+class SphereProblem:
+    """Sphere of `radius` at the origin with strictly interior charges."""
+
+    radius: float
+    params: PhysicalParams
+    charges: ChargeSystem
+
+    def __post_init__(self):
+        if not self.radius > 0.0:
+            raise ValueError(f"radius must be positive, got {self.radius}")
+        if len(self.charges):
+            rho = np.linalg.norm(self.charges.positions, axis=1)
+            bad = np.flatnonzero(rho >= self.radius - 1e-9)
+            if bad.size:
+                raise ValueError(f"charge {bad[0]} at distance {rho[bad[0]]} is not strictly "
+                                 f"inside the sphere of radius {self.radius}")
+
+
+def legendre_table(nmax: int, x) -> np.ndarray:
+    """P_0..P_nmax(x) by the three-term recurrence; shape (nmax+1,) + x.shape."""
+    x = np.asarray(x, dtype=float)
+    out = np.empty((nmax + 1,) + x.shape)
+    out[0] = 1.0
+    if nmax >= 1:
+        out[1] = x
+    for n in range(1, nmax):
+        out[n + 1] = ((2 * n + 1) * x * out[n] - n * out[n - 1]) / (n + 1)
+    return out
+
+
+def bessel_log_derivative(nmax: int, x: float) -> np.ndarray:
+    """x k_n'(x)/k_n(x), n = 0..nmax, through tau_n = k_n/k_{n-1} (never overflows);
+    x = 0 is the Laplace limit -(n+1) (kirkwood.py:92-110)."""
+    if x < 0.0:
+        raise ValueError(f"argument must be nonnegative, got {x}")
+    if x == 0.0:
+        return -np.arange(1.0, nmax + 2.0)
+    out = np.empty(nmax + 1)
+    out[0] = -(1.0 + x)
+    tau = 1.0 + 1.0 / x
+    for n in range(1, nmax + 1):
+        out[n] = -x / tau - (n + 1)
+        tau = 1.0 / tau + (2 * n + 1) / x
+    return out
+
+
+@dataclass(frozen=True)
+class KirkwoodSolution:
+    energy: float
+    phi: Callable[[np.ndarray], np.ndarray]
+    dphi_dn: Callable[[np.ndarray], np.ndarray]
+    tail_ratio: float
+    converged: bool
+    n_terms: int
+
+
+def _directions(v):
+    r = np.linalg.norm(v, axis=1)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        u = np.where(r[:, None] > 0.0, v / r[:, None], 0.0)
+    return r, u
+
+
+def kirkwood_series(problem: SphereProblem, n_terms: int = 40) -> KirkwoodSolution:
+    """Multipole solution for arbitrary interior charges (kirkwood.py:159-220)."""
+    if n_terms < 1:
+        raise ValueError(f"n_terms must be >= 1, got {n_terms}")
+    nmax = n_terms - 1
+    a, p = problem.radius, problem.params
+    q = problem.charges.charges
+    rho, units = _directions(problem.charges.positions)
+    n = np.arange(nmax + 1, dtype=float)
+    ell = bessel_log_derivative(nmax, p.kappa * a)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rpow = np.where(rho[:, None] > 0.0, rho[:, None] ** n[None, :], 0.0)
+    rpow[:, 0] = 1.0
+    alpha = q[:, None] * rpow / (FOUR_PI * p.eps1)
+    reac = alpha * (a ** -(2 * n + 1.0) * (p.eps2 * ell + (n + 1) * p.eps1) / (n * p.eps1 - p.eps2 * ell))
+    # E = 1/2 sum_j q_j phi_reac(y_j): P_n(u_j . u_k) for all charge pairs at once
+    pn = legendre_table(nmax, np.clip(units @ units.T, -1.0, 1.0)) if len(q) else np.zeros((nmax + 1, 0, 0))
+    energy = 0.0
+    for j in range(len(q)):
+        energy += 0.5 * q[j] * float((reac * rpow[j][None, :] * pn[:, :, j].T).sum())
+    energy *= FOUR_PI * KCAL_MOL_PER_E2_ANG
+    coef_phi = alpha * a ** -(n + 1.0) + reac * a**n
+    coef_dphi = -(n + 1.0) * alpha * a ** -(n + 2.0) + n * reac * a ** (n - 1.0)
+
+    def trace(coef):
+        def evaluate(points):
+            pts = np.asarray(points, dtype=float)
+            single = pts.ndim == 1
+            pts = pts.reshape(-1, 3)
+            _, rad = _directions(pts)
+            cos = rad @ units.T  # (m, nc)
+            cos[:, rho == 0.0] = 1.0
+            out = np.einsum("kn,nmk->m", coef, legendre_table(nmax, cos))
+            return out[0] if single else out
+
+        return evaluate
+
+    if nmax >= 1 and len(q):
+        last, prev = np.abs(coef_phi[:, nmax]), np.abs(coef_phi[:, nmax - 1])
+        tail = float(np.where(last > 0.0, last / np.maximum(prev, 1e-300), 0.0).max())
+    else:
+        tail = 1.0 if np.abs(coef_phi).max(initial=0.0) > 0.0 else 0.0
+    return KirkwoodSolution(energy=energy, phi=trace(coef_phi), dphi_dn=trace(coef_dphi),
+                            tail_ratio=tail, converged=tail <= 0.99, n_terms=n_terms)
+
+
+def kirkwood_centered(problem: SphereProblem):
+    """Closed form for one charge at the centre (kirkwood.py:223-263):
+    returns (E_sol, phi(points), dphi_dn(points)) with constant traces."""
+    if len(problem.charges) != 1:
+        raise NotCenteredError(f"closed form needs exactly one centered charge, got "
+                               f"{len(problem.charges)}; use kirkwood_series")
+    if float(np.linalg.norm(problem.charges.positions[0])) > 1e-12:
+        raise NotCenteredError("closed form needs the charge at the center; use kirkwood_series")
+    a, p = problem.radius, problem.params
+    q = float(problem.charges.charges[0])
+    screen = 1.0 + p.kappa * a
+    energy = KCAL_MOL_PER_E2_ANG * q * q / (2.0 * a) * (1.0 / (p.eps2 * screen) - 1.0 / p.eps1)
+
+    def const(value):
+        def fn(points):
+            pts = np.asarray(points, dtype=float)
+            return value if pts.ndim == 1 else np.full(pts.shape[0], value)
+
+        return fn
+
+    return (energy, const(q / (FOUR_PI * p.eps2 * a * screen)),
+            const(-q / (FOUR_PI * p.eps1 * a * a)))

@@ -159,12 +159,42 @@ def msms_case():
     print("msms: done", flush=True)
 
 
+def kirkwood_case():
+    """kirkwood_series / kirkwood_centered of the reference (kirkwood.py:159-263)."""
+    from pbbem.kirkwood import kirkwood_centered
+
+    c2 = baseline_config(2)
+    pts = c2.mesh.vertices
+    out = {"points": pts}
+    cases = {
+        "c2": (c2.charges.positions, c2.charges.charges, 1.0, 80.0, 0.1257, 2.0),
+        "ecc": (np.array([[0.0, 0.0, 1.7]]), np.array([1.0]), 2.0, 80.0, 0.5, 2.0),
+        "lap": (c2.charges.positions[:3], np.array([1.0, -0.5, 0.25]), 4.0, 80.0, 0.0, 2.0),
+    }
+    for tag, (pos, q, e1, e2, kap, a) in cases.items():
+        sph = SphereProblem(radius=a, params=rk.PhysicalParams(e1, e2, kap),
+                            charges=RCharges(positions=pos, charges=q))
+        ks = kirkwood_series(sph, n_terms=40)
+        out[tag + "_in"] = np.concatenate([pos.ravel(), q, [e1, e2, kap, a]])
+        out[tag + "_energy"] = np.array(ks.energy)
+        out[tag + "_phi"] = ks.phi(a / 2.0 * pts)
+        out[tag + "_dphi"] = ks.dphi_dn(a / 2.0 * pts)
+        out[tag + "_tail"] = np.array([ks.tail_ratio, float(ks.converged)])
+    sph = SphereProblem(radius=2.0, params=rk.PhysicalParams(1.0, 80.0, 0.1257),
+                        charges=RCharges(positions=[[0.0, 0.0, 0.0]], charges=[1.0]))
+    e, phi, dphi = kirkwood_centered(sph)
+    out["centered"] = np.array([e, phi(np.array([0.0, 0.0, 2.0])), dphi(np.array([0.0, 0.0, 2.0]))])
+    np.savez_compressed(os.path.join(HERE, "kirkwood.npz"), **out)
+    print("kirkwood: done", flush=True)
+
+
 def main():
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
             globals()[name]()
         return
     msms_case()
+    kirkwood_case()
     kernel_table()
     degenerate_case()
     star = StarShape.from_seed(16.0, seed=3)

@@ -246,3 +246,27 @@ def test_large_config_rows_vs_oracle(index):
         r1, r2 = O.rows(o, u, lo, hi)
         assert rel_l2(full[lo:hi], r1) <= MATVEC_TOL
         assert rel_l2(full[T + lo:T + hi], r2) <= MATVEC_TOL
+
+
+def test_sphere_solves_against_kirkwood():
+    """Configs 1-2 validated against the analytic series."""
+    from paper_1301_5914_b200 import surface_potential_error
+    from paper_1301_5914_b200.kirkwood import SphereProblem, kirkwood_series
+    from paper_1301_5914_b200.surfaces import baseline_config
+
+    errs = []
+    for level in (2, 3, 4):
+        cfg = baseline_config(1, level=level)
+        params = PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa)
+        prob, sol = solve(cfg.mesh, params, cfg.charges, SolverConfig(restart=cfg.restart, workers=1))
+        ks = kirkwood_series(SphereProblem(2.0, params, cfg.charges), 40)
+        errs.append(surface_potential_error(sol.phi, ks.phi(prob.colloc_pos)))
+        assert abs(solvation_energy(prob, sol) - ks.energy) <= 1e-2 * abs(ks.energy)
+    assert errs[0] > errs[1] > errs[2] and errs[1] < 1e-4  # refinement converges
+    cfg = baseline_config(2)
+    params = PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa)
+    prob, sol = solve(cfg.mesh, params, cfg.charges, SolverConfig(restart=cfg.restart, workers=1))
+    ks = kirkwood_series(SphereProblem(2.0, params, cfg.charges), 40)
+    assert ks.converged
+    assert surface_potential_error(sol.phi, ks.phi(prob.colloc_pos)) < 5e-3
+    assert abs(solvation_energy(prob, sol) - ks.energy) <= 5e-3 * abs(ks.energy)
