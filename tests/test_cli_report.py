@@ -67,6 +67,7 @@ def test_cli_solve_and_convergence(tmp_path, capsys):
     rep = reports_from_json(out.read_text())[0]
     assert rep.energy_kcal == pytest.approx(-82.18921350940137, rel=1e-8)
     assert rep.iterations == 6 and rep.matvecs == 8 and rep.phi_error < 1e-4
+    assert "E_sol = -82.1892" in capsys.readouterr().out  # summary line when --out is given
     assert main(["convergence", "--levels", "2,3", "--kappa", "0.1257", "--format", "csv"]) == 0
     reps = reports_from_csv(capsys.readouterr().out)
     assert len(reps) == 2 and reps[1].phi_error < reps[0].phi_error and reps[1].observed_order > 0
