@@ -343,7 +343,7 @@ def incident_pairs(faces, nv):
 
 
 def discretize(vertices, normals, faces, eps1, eps2, kappa, qpos=None, q=None,
-               scheme="hobi", duffy_n=4, check=True):
+               scheme="hobi", duffy_n=4, check=True, rule=None):
     """Build the caches of solver.py:165-266 (HOBI) or the flat LOBI ones (:177-186)."""
     vertices = np.asarray(vertices, dtype=float)
     normals = np.asarray(normals, dtype=float)
@@ -376,7 +376,7 @@ def discretize(vertices, normals, faces, eps1, eps2, kappa, qpos=None, q=None,
         raise OracleGeometryError(f"face {s // 3}: {_Fail.MESSAGES[int(code[s])]}")
     P = P.reshape(nf, 3, 10, 3)
     N = N.reshape(nf, 3, 10, 3)
-    rpts, rwts = conical_rule()
+    rpts, rwts = conical_rule() if rule is None else (np.asarray(rule[0], float), np.asarray(rule[1], float))
     dpts, dwts = duffy_points(duffy_n)
     prob.reg_pos, prob.reg_nrm, jac = frames(P[:, 0], N[:, 0], rpts)
     prob.reg_w = rwts[None, :] * jac

@@ -50,10 +50,12 @@ def _counted(op):
 
 
 def case(name, mesh, charges, eps1, eps2, kappa, *, restart=None, caches=False, solve=False,
-         kirkwood_radius=None, u_seed=7, workers=8):
+         kirkwood_radius=None, u_seed=7, workers=8, scheme="hobi", duffy=4, rule=None):
     t0 = time.time()
     params = rk.PhysicalParams(eps1, eps2, kappa)
-    cfg = rs.SolverConfig(scheme="hobi", workers=workers, restart=restart or 100)
+    extra = {} if rule is None else {"regular_rule": rule}
+    cfg = rs.SolverConfig(scheme=scheme, workers=workers, restart=restart or 100, duffy_points=duffy,
+                          **extra)
     prob = rs.discretize(_ref_mesh(mesh), params, _ref_charges(charges), cfg)
     out = dict(vertices=mesh.vertices, normals=mesh.normals, faces=mesh.faces,
                qpos=charges.positions, q=charges.charges,
@@ -72,6 +74,11 @@ def case(name, mesh, charges, eps1, eps2, kappa, *, restart=None, caches=False, 
             out["matvecs"] = np.array(count[0])
             out["restart"] = np.array(cfg.restart)
             out["energy"] = np.array(rs.solvation_energy(prob, sol))
+    out["duffy"] = np.array(duffy)
+    out["scheme"] = np.array(scheme)
+    if rule is not None:
+        out["rule_points"], out["rule_weights"] = rule.points, rule.weights
+        out["rule_degree"] = np.array(rule.degree)
     if caches:
         for k in ("reg_pos", "reg_nrm", "reg_w", "reg_bary", "pair_vertex", "pair_face",
                   "pair_gverts", "pair_starts", "duf_pos", "duf_nrm", "duf_w", "duf_bary"):
@@ -188,6 +195,18 @@ def kirkwood_case():
     print("kirkwood: done", flush=True)
 
 
+def variants_case():
+    """Other quadrature choices and the LOBI solve (SolverConfig knobs, solver.py:58-68)."""
+    from pbbem.quadrature import duffy_rule
+
+    star = StarShape.from_seed(16.0, seed=3)
+    few = star.interior_charges(20, seed=5)
+    case("star_l1_duffy6", star.surface(1), few, 2.0, 80.0, 0.5, caches=True, duffy=6)
+    case("star_l2_rule9", star.surface(2), few, 4.0, 80.0, 0.1257, caches=True, duffy=3,
+         rule=duffy_rule(3), solve=True, restart=15)
+    case("star_l2_lobi", star.surface(2), few, 2.0, 80.0, 0.1257, solve=True, restart=20, scheme="lobi")
+
+
 def main():
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -195,6 +214,7 @@ def main():
         return
     msms_case()
     kirkwood_case()
+    variants_case()
     kernel_table()
     degenerate_case()
     star = StarShape.from_seed(16.0, seed=3)

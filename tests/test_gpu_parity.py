@@ -270,3 +270,78 @@ def test_sphere_solves_against_kirkwood():
     assert ks.converged
     assert surface_potential_error(sol.phi, ks.phi(prob.colloc_pos)) < 5e-3
     assert abs(solvation_energy(prob, sol) - ks.energy) <= 5e-3 * abs(ks.energy)
+
+
+@pytest.mark.parametrize("name", ["star_l1_duffy6", "star_l2_rule9"])
+def test_quadrature_variants_bit_exact_caches_and_matvec(name):
+    """SolverConfig.duffy_points / regular_rule other than the defaults (solver.py:67-68)."""
+    from paper_1301_5914_b200 import TriangleRule
+
+    g = golden(name)
+    kw = {"duffy_points": int(g["duffy"])}
+    if "rule_points" in g:
+        kw["regular_rule"] = TriangleRule(g["rule_points"], g["rule_weights"], "custom",
+                                          int(g["rule_degree"]))
+    prob = _problem(g, **kw)
+    for key in ("reg_pos", "reg_nrm", "reg_w", "duf_pos", "duf_nrm", "duf_w"):
+        assert np.array_equal(getattr(prob, key), g[key]), key
+    assert rel_l2(matvec_hobi(prob, g["u"]), g["Au"]) <= MATVEC_TOL
+    if "phi" in g:
+        cfg = SolverConfig(workers=1, restart=int(g["restart"]), **kw)
+        with make_operator(prob, cfg) as op:
+            sol = gmres_solve(op, assemble_rhs(prob), cfg)
+        assert sol.iterations == int(g["iterations"])
+        assert rel_l2(sol.phi, g["phi"]) <= SOLVE_TOL
+        e = solvation_energy(prob, sol)
+        assert abs(e - float(g["energy"])) <= SOLVE_TOL * abs(float(g["energy"]))
+
+
+def test_lobi_solve_matches_reference():
+    g = golden("star_l2_lobi")
+    prob = _problem(g, scheme="lobi")
+    assert rel_l2(matvec_lobi(prob, g["u"]), g["Au"]) <= MATVEC_TOL
+    cfg = SolverConfig(scheme="lobi", workers=1, restart=int(g["restart"]))
+    with make_operator(prob, cfg) as op:
+        sol = gmres_solve(op, assemble_rhs(prob), cfg)
+    assert sol.iterations == int(g["iterations"]) and sol.matvecs == int(g["matvecs"])
+    assert rel_l2(sol.phi, g["phi"]) <= SOLVE_TOL
+    e = solvation_energy(prob, sol)
+    assert abs(e - float(g["energy"])) <= SOLVE_TOL * abs(float(g["energy"]))
+
+
+def test_gpu_operator_nonconvergence_and_empty_charges():
+    g = golden("star_l2")
+    prob = _problem(g)
+    cfg = SolverConfig(workers=1, tolerance=1e-14, max_iterations=3, restart=2)
+    with make_operator(prob, cfg) as op:
+        with pytest.raises(GmresNonConvergence) as info:
+            gmres_solve(op, assemble_rhs(prob), cfg)
+    assert 0.0 < info.value.best_residual < 1.0
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    empty = discretize(mesh, PhysicalParams(*g["params"]), ChargeSystem(np.zeros((0, 3)), []),
+                       SolverConfig())
+    assert np.all(assemble_rhs(empty) == 0.0)
+    with make_operator(empty, SolverConfig()) as op:
+        sol = gmres_solve(op, assemble_rhs(empty), SolverConfig())
+    assert sol.iterations == 0 and np.all(sol.vector == 0.0)
+    assert solvation_energy(empty, sol) == 0.0
+
+
+def test_rhs_singularity_reported():
+    from paper_1301_5914_b200 import SingularityError
+
+    g = golden("star_l2")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    prob = discretize(mesh, PhysicalParams(*g["params"]),
+                      ChargeSystem([[0.0, 0.0, 0.0], g["vertices"][5]], [1.0, 1.0]), SolverConfig())
+    with pytest.raises(SingularityError, match="surface point 5 coincides with charge 1"):
+        assemble_rhs(prob)
+
+
+def test_wrong_length_and_scheme_mismatch():
+    g = golden("star_l2")
+    prob = _problem(g)
+    with pytest.raises(ValueError, match="length"):
+        matvec_hobi(prob, np.zeros(prob.n_unknowns + 2))
+    with pytest.raises(ValueError):
+        matvec_lobi(prob, np.zeros(prob.n_unknowns))

@@ -121,3 +121,23 @@ def test_oracle_row_split_bitwise():
         parts = [O.rows(p, u, lo, hi) for lo, hi in O.partition(T, w)]
         got = np.concatenate([np.concatenate([a for a, _ in parts]), np.concatenate([b for _, b in parts])])
         assert np.array_equal(got, full)
+
+
+@pytest.mark.parametrize("name", ["star_l1_duffy6", "star_l2_rule9"])
+def test_oracle_quadrature_variants(name):
+    g = golden(name)
+    rule = (g["rule_points"], g["rule_weights"]) if "rule_points" in g else None
+    p = O.discretize(g["vertices"], g["normals"], g["faces"], *g["params"], g["qpos"], g["q"],
+                     duffy_n=int(g["duffy"]), rule=rule)
+    for key in ("reg_pos", "reg_nrm", "reg_w", "duf_pos", "duf_nrm", "duf_w"):
+        assert np.array_equal(getattr(p, key), g[key]), key
+    assert rel_l2(O.matvec(p, g["u"]), g["Au"]) <= 1e-14
+
+
+def test_oracle_lobi_solve():
+    g = golden("star_l2_lobi")
+    p = _disc(g, scheme="lobi")
+    assert rel_l2(O.matvec(p, g["u"]), g["Au"]) <= 1e-14
+    phi, dphi, its, _, nmv = O.solve(p, restart=int(g["restart"]), workers=1)
+    assert its == int(g["iterations"]) and nmv == int(g["matvecs"])
+    assert abs(O.energy(p, phi, dphi) - float(g["energy"])) <= 1e-12 * abs(float(g["energy"]))
