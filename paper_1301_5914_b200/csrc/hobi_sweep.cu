@@ -275,19 +275,32 @@ __global__ void source_weights_kernel(const double* __restrict__ u, int64_t nt,
 }
 
 // K-D: fixed-order group reduction + Duffy swap (solver.py:362-363) + diagonal
-// (solver.py:365-366).  Row v of [lo, hi) is written to o1[v-lo], o2[v-lo].
-__global__ void epilogue_kernel(const double* __restrict__ part, int64_t ldp, int n_groups,
-                                const double* __restrict__ corr, const int* __restrict__ pair_starts,
-                                const double* __restrict__ u, int64_t nt, int64_t lo, int64_t hi,
-                                double diag1, double diag2, double* __restrict__ o1,
-                                double* __restrict__ o2) {
-  int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (v >= hi) return;
-  double acc1 = part[v], acc2 = part[ldp + v];
-  for (int g = 1; g < n_groups; ++g) {
-    acc1 += part[(2 * (int64_t)g) * ldp + v];
-    acc2 += part[(2 * (int64_t)g + 1) * ldp + v];
+// (solver.py:365-366).  A block covers 32 consecutive rows (threadIdx.x, so
+// every partial-sum load is a coalesced 256-byte row segment) x 8 group
+// slices (threadIdx.y: groups y, y+8, ...); the 8 slice sums are folded in a
+// fixed order, so each row's result is independent of the row split.
+// Row v of [lo, hi) is written to o1[v-lo], o2[v-lo].
+constexpr int kEpiRows = 32, kEpiSlices = 8;
+__global__ void __launch_bounds__(kEpiRows* kEpiSlices) epilogue_kernel(
+    const double* __restrict__ part, int64_t ldp, int n_groups, const double* __restrict__ corr,
+    const int* __restrict__ pair_starts, const double* __restrict__ u, int64_t nt, int64_t lo,
+    int64_t hi, double diag1, double diag2, double* __restrict__ o1, double* __restrict__ o2) {
+  __shared__ double s1[kEpiSlices][kEpiRows], s2[kEpiSlices][kEpiRows];
+  const int64_t v = lo + (int64_t)blockIdx.x * kEpiRows + threadIdx.x;
+  const int64_t vv = v < hi ? v : hi - 1;
+  double a1 = 0.0, a2 = 0.0;
+  for (int g = threadIdx.y; g < n_groups; g += kEpiSlices) {
+    a1 += part[(2 * (int64_t)g) * ldp + vv];
+    a2 += part[(2 * (int64_t)g + 1) * ldp + vv];
   }
+  s1[threadIdx.y][threadIdx.x] = a1;
+  s2[threadIdx.y][threadIdx.x] = a2;
+  __syncthreads();
+  if (threadIdx.y != 0 || v >= hi) return;
+  double acc1 = ((s1[0][threadIdx.x] + s1[1][threadIdx.x]) + (s1[2][threadIdx.x] + s1[3][threadIdx.x])) +
+                ((s1[4][threadIdx.x] + s1[5][threadIdx.x]) + (s1[6][threadIdx.x] + s1[7][threadIdx.x]));
+  double acc2 = ((s2[0][threadIdx.x] + s2[1][threadIdx.x]) + (s2[2][threadIdx.x] + s2[3][threadIdx.x])) +
+                ((s2[4][threadIdx.x] + s2[5][threadIdx.x]) + (s2[6][threadIdx.x] + s2[7][threadIdx.x]));
   if (corr) {
     double c1 = 0.0, c2 = 0.0;
     for (int p = pair_starts[v]; p < pair_starts[v + 1]; ++p) {
@@ -455,7 +468,9 @@ std::vector<int2> make_groups(int n_src_tiles, int64_t tiles8) {
   std::vector<int2> g;
   if (n_src_tiles <= 0) return g;
   const int64_t want = std::max<int64_t>(1, (16 * 2 * 148 + tiles8 - 1) / tiles8);
-  const int B = (int)std::max<int64_t>(1, (n_src_tiles + want - 1) / want);
+  // at least 4 tiles (256 sources) per group: the partial sums then cost
+  // <= 1/16 B per pair of HBM traffic
+  const int B = (int)std::max<int64_t>(std::min(4, n_src_tiles), (n_src_tiles + want - 1) / want);
   std::vector<int> tail;
   int tail_sum = 0;
   for (int s = 1; s < B; s *= 2) {
@@ -527,7 +542,7 @@ int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi,
     corr = c->corr.p;
     starts = c->pair_starts.p;
   }
-  epilogue_kernel<<<nblk(hi - lo, 256), 256, 0, c->stream>>>(
+  epilogue_kernel<<<nblk(hi - lo, kEpiRows), dim3(kEpiRows, kEpiSlices), 0, c->stream>>>(
       c->part.p, c->nt_pad, c->n_groups, corr, starts, u_dev, c->nt, lo, hi, c->phys.diag1,
       c->phys.diag2, o1, o2);
   c->launches++;
