@@ -331,6 +331,7 @@ def run_ours(a):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    prob.close()  # release the device context and its NCCL communicator before torch's
     if world > 1:
         import torch.distributed as dist
 

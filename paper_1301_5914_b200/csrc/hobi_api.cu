@@ -621,6 +621,7 @@ int hobi_sweep_variant(hobi_ctx* c, int variant, int* count, char* name, int nam
   if (variant >= 0) {
     if (variant >= sweep_variant_count()) return fail(HOBI_ERR_VALUE, "no such sweep variant");
     c->sweep_variant = variant;
+    c->variant_pinned = true;
   }
   if (name && name_len > 0) {
     snprintf(name, name_len, "%s", sweep_variant_name(c->sweep_variant));

@@ -122,6 +122,7 @@ struct hobi_ctx {
   int64_t launches = 0;
   bool timing = true;
   int sweep_variant = 7;  // index into the sweep tuning table (hobi_sweep.cu): R6_minb2_unroll1
+  bool variant_pinned = false;  // set by hobi_sweep_variant: no small-problem switch
 };
 
 namespace hobi {

@@ -389,6 +389,7 @@ static const SweepVariant kVariants[] = {
 };
 #undef HOBI_V
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+constexpr int kSmallVariant = 3;  // R1_minb8_unroll2
 
 int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_t t1, bool full,
                  double* part, int64_t ldp, const int2* groups, int n_groups) {
@@ -400,7 +401,12 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
     if (self)
       fn = sweep_kernel<kScreened, true, true, kSweepR, 1, 2>;
     else if (full) {
-      const SweepVariant& v = kVariants[c->sweep_variant];
+      int vi = c->sweep_variant;
+      // small problems: if the tuned tile leaves too few work items for 148
+      // SMs, use 128-row tiles (same sums bitwise, more parallelism)
+      const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * kVariants[vi].r) * n_groups;
+      if (!c->variant_pinned && items < 2 * 296) vi = kSmallVariant;
+      const SweepVariant& v = kVariants[vi];
       fn = v.fn;
       r = v.r;
     } else
@@ -468,9 +474,10 @@ std::vector<int2> make_groups(int n_src_tiles, int64_t tiles8) {
   std::vector<int2> g;
   if (n_src_tiles <= 0) return g;
   const int64_t want = std::max<int64_t>(1, (16 * 2 * 148 + tiles8 - 1) / tiles8);
-  // at least 4 tiles (256 sources) per group: the partial sums then cost
-  // <= 1/16 B per pair of HBM traffic
-  const int B = (int)std::max<int64_t>(std::min(4, n_src_tiles), (n_src_tiles + want - 1) / want);
+  // large problems get at least 4 tiles (256 sources) per group, so the
+  // partial sums cost <= 1/16 B of HBM traffic per pair
+  const int floor = n_src_tiles >= 1024 ? 4 : 1;
+  const int B = (int)std::max<int64_t>(floor, (n_src_tiles + want - 1) / want);
   std::vector<int> tail;
   int tail_sum = 0;
   for (int s = 1; s < B; s *= 2) {

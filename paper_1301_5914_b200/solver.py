@@ -170,7 +170,13 @@ class DiscretizedProblem:
 
     @property
     def handle(self):
+        if not self._h.ptr:
+            raise ValueError("problem has been closed")
         return self._h.ptr
+
+    def close(self):
+        """Free the device caches (and the NCCL communicator) now rather than at GC."""
+        self._h.__del__()
 
     @property
     def n_collocation(self) -> int:
