@@ -55,6 +55,8 @@ def _args():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0, help="rows per CPU sample (0 = auto)")
+    ap.add_argument("--gather", choices=("nccl", "p2p"), default=os.environ.get("HOBI_GATHER", "nccl"),
+                    help="N>1 row gather: ncclAllGather, or the fused epilogue + NVLink peer stores")
     return ap.parse_args()
 
 
@@ -193,6 +195,7 @@ def run_reference(a):
 
 def run_ours(a):
     rank, world, local = _dist()
+    os.environ["HOBI_GATHER"] = a.gather
     if world != a.gpus:
         a.gpus = world
     if world > 1:
@@ -310,7 +313,8 @@ def run_ours(a):
             traffic = None
     if rank == 0:
         conf = _workload(cfg, nv, nf, nq)
-        conf["parallelism"] = f"row split x{world} + NCCL allgather" if world > 1 else "single GPU"
+        conf["parallelism"] = (f"row split x{world} + " + ("NCCL allgather" if a.gather == "nccl" else
+                               "fused epilogue/NVLink peer-store gather")) if world > 1 else "single GPU"
         line = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,

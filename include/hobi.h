@@ -136,6 +136,16 @@ int hobi_kernel_values(int device, const double* d, const double* nx, const doub
  */
 int hobi_comm_unique_id(unsigned char id[128]);
 int hobi_comm_init(hobi_ctx* ctx, const unsigned char id[128], int nranks, int rank);
+/*
+ * Opt-in alternative to the NCCL allgather: the epilogue kernel stores every
+ * finished row directly into all ranks' receive buffers over NVLink (CUDA IPC
+ * peer memory) and signals arrival with system-scope atomics; a wait kernel
+ * hands the gathered vector on.  After hobi_comm_init, every rank calls
+ * hobi_comm_p2p_handle, the host all-gathers the 64-byte handles (rank
+ * order), and every rank calls hobi_comm_p2p_open with all of them.
+ */
+int hobi_comm_p2p_handle(hobi_ctx* ctx, unsigned char handle[64]);
+int hobi_comm_p2p_open(hobi_ctx* ctx, const unsigned char* handles, int nranks, int rank);
 /* Single-GPU emulation of an nranks-way split (same buffers, same gather
  * layout and permutation kernel, no NCCL): for determinism tests. */
 int hobi_emulate_ranks(hobi_ctx* ctx, int nranks);

@@ -53,6 +53,8 @@ SIGNATURES = {
     "hobi_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
     "hobi_comm_init": (C.c_int, [_ctxp, C.POINTER(C.c_ubyte), C.c_int, C.c_int]),
     "hobi_emulate_ranks": (C.c_int, [_ctxp, C.c_int]),
+    "hobi_comm_p2p_handle": (C.c_int, [_ctxp, C.POINTER(C.c_ubyte)]),
+    "hobi_comm_p2p_open": (C.c_int, [_ctxp, C.POINTER(C.c_ubyte), C.c_int, C.c_int]),
     "hobi_timing_reset": (C.c_int, [_ctxp]),
     "hobi_timing": (C.c_int, [_ctxp, _dp, _i64p, _i64p]),
     "hobi_pairs_per_matvec": (C.c_int, [_ctxp, _dp]),

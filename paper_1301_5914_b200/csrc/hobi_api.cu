@@ -354,6 +354,8 @@ int hobi_destroy(hobi_ctx* c) {
   cudaSetDevice(c->device);
   if (c->comm.nccl && nccl::api().loaded) nccl::api().destroy(c->comm.nccl);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->comm.opened) cudaIpcCloseMemHandle(p);
+  if (c->stream) cudaStreamSynchronize(c->stream);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -544,6 +546,48 @@ int hobi_comm_init(hobi_ctx* c, const unsigned char id[128], int nranks, int ran
   int rc = nccl::check(a.init_rank(&c->comm.nccl, nranks, u, rank), "ncclCommInitRank");
   if (rc) return rc;
   return setup_gather(c, nranks);
+}
+
+int hobi_comm_p2p_handle(hobi_ctx* c, unsigned char handle[64]) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  // two (2 nt) receive buffers + arrival counters [parity][source rank]
+  if (c->comm.nranks > kMaxRanks) return fail(HOBI_ERR_VALUE, "P2P gather supports at most 64 ranks");
+  const size_t n = 4 * (size_t)c->nt + 2 * kMaxRanks;
+  if (c->p2p_area.alloc(n)) return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemset(c->p2p_area.p, 0, n * sizeof(double)));
+  cudaIpcMemHandle_t h;
+  HOBI_CUDA(cudaIpcGetMemHandle(&h, c->p2p_area.p));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle, &h, 64);
+  return 0;
+}
+
+int hobi_comm_p2p_open(hobi_ctx* c, const unsigned char* handles, int nranks, int rank) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (!c->p2p_area.p) return fail(HOBI_ERR_STATE, "hobi_comm_p2p_handle must be called first");
+  if (nranks != c->comm.nranks || rank != c->comm.rank)
+    return fail(HOBI_ERR_STATE, "P2P ranks differ from the communicator (call hobi_comm_init first)");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  std::vector<double*> ptrs(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == rank) {
+      ptrs[r] = c->p2p_area.p;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 64 * (size_t)r, 64);
+    void* p = nullptr;
+    HOBI_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->comm.opened.push_back(p);
+    ptrs[r] = static_cast<double*>(p);
+  }
+  if (c->p2p_peers.alloc(nranks) || c->p2p_done.alloc(1)) return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemcpy(c->p2p_peers.p, ptrs.data(), nranks * sizeof(double*), cudaMemcpyHostToDevice));
+  HOBI_CUDA(cudaMemset(c->p2p_done.p, 0, sizeof(unsigned)));
+  c->comm.p2p = true;
+  c->comm.epoch = 0;
+  return 0;
 }
 
 int hobi_emulate_ranks(hobi_ctx* c, int nranks) {

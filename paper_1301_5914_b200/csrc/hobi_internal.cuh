@@ -21,6 +21,7 @@ constexpr int kTargetTile = kSweepThreads * kSweepR;
 constexpr int kSrcTile = 64;        // sources per shared-memory stage
 constexpr int kSrcStride = 12;      // doubles per source record
 constexpr int kStages = 4;          // TMA bulk-copy pipeline depth
+constexpr int kMaxRanks = 64;      // P2P gather: arrival counters per buffer parity
 constexpr int kExpShift = 11;
 constexpr int kExpTable = 1 << kExpShift;  // 2^(j/2048) table for the FP64 exp
 
@@ -75,6 +76,10 @@ struct Comm {
   int nranks = 1;
   int rank = 0;
   bool emulated = false;
+  // fused epilogue + NVLink peer-store gather (hobi_comm_p2p_*)
+  bool p2p = false;
+  uint64_t epoch = 0;                 // operator applications gathered so far
+  std::vector<void*> opened;          // peer areas opened through CUDA IPC
 };
 
 }  // namespace hobi
@@ -110,6 +115,11 @@ struct hobi_ctx {
   hobi::DevBuf<double> corr;                 // (3nf, 2) Duffy-minus-regular per pair
   hobi::DevBuf<double> u, out;               // (2nt)
   hobi::DevBuf<double> gather_send, gather_recv;  // (2*m), (nranks*2*m)
+  // P2P area: two (2*nt) receive buffers (epoch parity) + 2 arrival counters,
+  // exported to the peers through CUDA IPC; p2p_peers[r] = rank r's area.
+  hobi::DevBuf<double> p2p_area;
+  hobi::DevBuf<double*> p2p_peers;
+  hobi::DevBuf<unsigned> p2p_done;
   int64_t gather_m = 0;
   hobi::Comm comm;
 

@@ -314,6 +314,84 @@ __global__ void __launch_bounds__(kEpiRows* kEpiSlices) epilogue_kernel(
   o2[v - lo] = __dsub_rn(__dmul_rn(diag2, u[nt + v]), acc2);
 }
 
+// Fused epilogue + gather over NVLink (P2P mode): the same fixed-order row
+// reduction as epilogue_kernel, but every finished row is stored straight
+// into all ranks' receive buffers (final layout, phi rows then dphi rows) by
+// peer stores; the last block to finish fences and bumps every rank's
+// arrival counter for this epoch parity with a system-scope atomic.
+__global__ void __launch_bounds__(kEpiRows* kEpiSlices) epilogue_p2p_kernel(
+    const double* __restrict__ part, int64_t ldp, int n_groups, const double* __restrict__ corr,
+    const int* __restrict__ pair_starts, const double* __restrict__ u, int64_t nt, int64_t lo,
+    int64_t hi, double diag1, double diag2, double* const* __restrict__ peers, int nranks, int rank,
+    int parity, unsigned* __restrict__ done) {
+  __shared__ double s1[kEpiSlices][kEpiRows], s2[kEpiSlices][kEpiRows];
+  const int64_t v = lo + (int64_t)blockIdx.x * kEpiRows + threadIdx.x;
+  const int64_t vv = v < hi ? v : hi - 1;
+  double a1 = 0.0, a2 = 0.0;
+  for (int g = threadIdx.y; hi > lo && g < n_groups; g += kEpiSlices) {
+    a1 += part[(2 * (int64_t)g) * ldp + vv];
+    a2 += part[(2 * (int64_t)g + 1) * ldp + vv];
+  }
+  s1[threadIdx.y][threadIdx.x] = a1;
+  s2[threadIdx.y][threadIdx.x] = a2;
+  __syncthreads();
+  if (threadIdx.y == 0 && v < hi) {
+    double acc1 = ((s1[0][threadIdx.x] + s1[1][threadIdx.x]) + (s1[2][threadIdx.x] + s1[3][threadIdx.x])) +
+                  ((s1[4][threadIdx.x] + s1[5][threadIdx.x]) + (s1[6][threadIdx.x] + s1[7][threadIdx.x]));
+    double acc2 = ((s2[0][threadIdx.x] + s2[1][threadIdx.x]) + (s2[2][threadIdx.x] + s2[3][threadIdx.x])) +
+                  ((s2[4][threadIdx.x] + s2[5][threadIdx.x]) + (s2[6][threadIdx.x] + s2[7][threadIdx.x]));
+    double c1 = 0.0, c2 = 0.0;
+    for (int p = pair_starts[v]; p < pair_starts[v + 1]; ++p) {
+      c1 += corr[2 * (int64_t)p];
+      c2 += corr[2 * (int64_t)p + 1];
+    }
+    acc1 += c1;
+    acc2 += c2;
+    const double r1 = __dsub_rn(__dmul_rn(diag1, u[v]), acc1);
+    const double r2 = __dsub_rn(__dmul_rn(diag2, u[nt + v]), acc2);
+    const int64_t off = (int64_t)parity * 2 * nt;
+    for (int r = 0; r < nranks; ++r) {  // peer stores over NVLink (own buffer for r == rank)
+      peers[r][off + v] = r1;
+      peers[r][off + nt + v] = r2;
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const unsigned prev = atomicAdd(done, 1u);
+    if (prev == gridDim.x - 1) {  // last block: every row of this rank is out
+      __threadfence_system();
+      // counter (parity, this rank) in every rank's area: one writer per
+      // counter, so a rank running ahead can never stand in for a late one
+      for (int r = 0; r < nranks; ++r) {
+        unsigned long long* flag =
+            reinterpret_cast<unsigned long long*>(peers[r] + 4 * nt) + parity * kMaxRanks + rank;
+        atomicAdd_system(flag, 1ull);
+      }
+      *done = 0u;
+    }
+  }
+}
+
+// Wait until all ranks' rows of this epoch have arrived, then hand the
+// gathered vector to the caller's buffer.
+__global__ void p2p_wait_copy_kernel(const double* __restrict__ area, int64_t nt, int nranks, int parity,
+                                     unsigned long long target, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* flag =
+        reinterpret_cast<volatile unsigned long long*>(const_cast<double*>(area) + 4 * nt) +
+        parity * kMaxRanks;
+    for (int r = 0; r < nranks; ++r)
+      while (flag[r] < target) __nanosleep(64);
+    __threadfence_system();
+  }
+  __syncthreads();
+  const double* buf = area + (int64_t)parity * 2 * nt;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 2 * nt;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = __ldcv(buf + k);
+}
+
 // Gathered rank-major rows [r][2][m] -> out[0:nt] ++ out[nt:2nt].
 __global__ void permute_kernel(const double* __restrict__ recv, int64_t m, int64_t nt, int nranks,
                                double* __restrict__ out) {
@@ -557,8 +635,37 @@ int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi,
   return 0;
 }
 
+// Row split with the gather fused into the epilogue (peer stores + arrival
+// counters) instead of ncclAllGather + permutation.
+static int matvec_p2p(hobi_ctx* c, const double* u_dev, double* out_dev) {
+  const int64_t lo = c->lo, hi = c->hi;
+  const int parity = (int)(c->comm.epoch & 1);
+  const unsigned long long target = c->comm.epoch / 2 + 1;  // arrivals per rank for this parity
+  int rc;
+  if (hi > lo) {
+    if ((rc = update_weights(c, u_dev))) return rc;
+    if ((rc = launch_sweep(c, c->tgt.p, c->nt_pad, lo, hi, true, c->part.p, c->nt_pad, c->groups.p,
+                           c->n_groups)))
+      return rc;
+    if ((rc = launch_singular(c, u_dev, c->h_pair_starts[lo], c->h_pair_starts[hi]))) return rc;
+  }
+  // an empty range still launches one block so this rank signals its arrival
+  const unsigned blocks = hi > lo ? nblk(hi - lo, kEpiRows) : 1;
+  epilogue_p2p_kernel<<<blocks, dim3(kEpiRows, kEpiSlices), 0, c->stream>>>(
+      c->part.p, c->nt_pad, c->n_groups, c->corr.p, c->pair_starts.p, u_dev, c->nt, lo, hi,
+      c->phys.diag1, c->phys.diag2, c->p2p_peers.p, c->comm.nranks, c->comm.rank, parity,
+      c->p2p_done.p);
+  p2p_wait_copy_kernel<<<std::max(1u, nblk(2 * c->nt, 1024)), 256, 0, c->stream>>>(
+      c->p2p_area.p, c->nt, c->comm.nranks, parity, target, out_dev);
+  c->launches += 2;
+  HOBI_CUDA(cudaGetLastError());
+  c->comm.epoch++;
+  return 0;
+}
+
 int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
   int rc;
+  if (c->comm.p2p) return matvec_p2p(c, u_dev, out_dev);
   if (c->comm.nranks == 1 && !c->comm.nccl)
     return matvec_rows_device(c, u_dev, 0, c->nt, out_dev, out_dev + c->nt);
   const int64_t m = c->gather_m;

@@ -14,6 +14,7 @@ same index map) plus the NCCL unique-id exchange over torch.distributed.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -56,7 +57,9 @@ def unpack_gathered(recv: np.ndarray, n: int, nranks: int) -> np.ndarray:
 
 def init_nccl_comm(handle, rank: int, world: int) -> None:
     """Create the library's NCCL communicator: rank 0 draws the unique id,
-    torch.distributed broadcasts the 128 bytes, every rank joins."""
+    torch.distributed broadcasts the 128 bytes, every rank joins.  With
+    HOBI_GATHER=p2p the gather is then switched to the fused epilogue +
+    NVLink peer-store path (init_p2p_gather)."""
     import torch.distributed as dist
 
     from . import _native as N
@@ -69,3 +72,24 @@ def init_nccl_comm(handle, rank: int, world: int) -> None:
     dist.broadcast_object_list(box, src=0)
     uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
     N.check(lib.hobi_comm_init(handle, uid, world, rank))
+    if os.environ.get("HOBI_GATHER", "nccl") == "p2p":
+        init_p2p_gather(handle, rank, world)
+
+
+def init_p2p_gather(handle, rank: int, world: int) -> None:
+    """Exchange the CUDA IPC handles of every rank's receive area (rank order)
+    and switch the operator's gather to peer stores from the epilogue."""
+    from . import _native as N
+
+    lib = N.load()
+    mine = (C.c_ubyte * 64)()
+    N.check(lib.hobi_comm_p2p_handle(handle, mine))
+    if world > 1:
+        import torch.distributed as dist
+
+        allh = [None] * world
+        dist.all_gather_object(allh, bytes(mine))
+    else:
+        allh = [bytes(mine)]
+    buf = (C.c_ubyte * (64 * world)).from_buffer_copy(b"".join(allh))
+    N.check(lib.hobi_comm_p2p_open(handle, buf, world, rank))

@@ -40,3 +40,36 @@ def test_single_rank_nccl_gather_path(monkeypatch):
     with make_operator(prob, cfg) as op:
         sol = gmres_solve(op, assemble_rhs(prob), cfg)
     assert sol.iterations == int(g["iterations"])
+
+
+def test_single_rank_p2p_fused_gather(monkeypatch):
+    """Fused epilogue + peer-store gather (HOBI_GATHER=p2p path) with one rank:
+    the kernel stores into the (own) receive area, bumps the arrival counter
+    and the wait kernel releases -- bitwise equal to the plain operator over
+    many epochs (both buffer parities) and through a full GMRES solve."""
+    from paper_1301_5914_b200 import (ChargeSystem, FlatMesh, PhysicalParams, SolverConfig,
+                                      discretize, gmres_solve, make_operator, matvec_hobi,
+                                      assemble_rhs)
+    from paper_1301_5914_b200 import _native as N
+    from paper_1301_5914_b200.distributed import init_p2p_gather
+
+    g = golden("star_l3")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    params = PhysicalParams(*g["params"])
+    charges = ChargeSystem(g["qpos"], g["q"])
+    plain = discretize(mesh, params, charges, SolverConfig(workers=1))
+    ref = matvec_hobi(plain, g["u"])
+    prob = discretize(mesh, params, charges, SolverConfig(workers=1))
+    lib = N.load()
+    uid = (C.c_ubyte * 128)()
+    N.check(lib.hobi_comm_init(prob.handle, uid, 1, 0))
+    init_p2p_gather(prob.handle, 0, 1)
+    for _ in range(5):
+        assert np.array_equal(matvec_hobi(prob, g["u"]), ref)
+    cfg = SolverConfig(workers=1, restart=int(g["restart"]))
+    with make_operator(prob, cfg) as op:
+        sol = gmres_solve(op, assemble_rhs(prob), cfg)
+    assert sol.iterations == int(g["iterations"])
+    with make_operator(plain, cfg) as op:
+        sol0 = gmres_solve(op, assemble_rhs(plain), cfg)
+    assert np.array_equal(sol.vector, sol0.vector)
