@@ -198,7 +198,8 @@ def run_ours(a):
     os.environ["HOBI_GATHER"] = a.gather
     if world != a.gpus:
         a.gpus = world
-    if world > 1:
+    use_dist = world > 1 or ("RANK" in os.environ and os.environ.get("HOBI_FORCE_NCCL") == "1")
+    if use_dist:
         import torch
         import torch.distributed as dist
 
@@ -229,13 +230,13 @@ def run_ours(a):
         hi = lo + base + (1 if rank < extra else 0)
 
     def barrier():
-        if world > 1:
+        if use_dist:
             import torch.distributed as dist
 
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
+        if not use_dist:
             return x
         import torch
         import torch.distributed as dist
@@ -336,7 +337,7 @@ def run_ours(a):
         }
         print(json.dumps(line), flush=True)
     prob.close()  # release the device context and its NCCL communicator before torch's
-    if world > 1:
+    if use_dist:
         import torch.distributed as dist
 
         dist.destroy_process_group()
