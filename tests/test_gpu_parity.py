@@ -345,3 +345,22 @@ def test_wrong_length_and_scheme_mismatch():
         matvec_hobi(prob, np.zeros(prob.n_unknowns + 2))
     with pytest.raises(ValueError):
         matvec_lobi(prob, np.zeros(prob.n_unknowns))
+
+
+def test_repeated_runs_and_all_sweep_variants_bitwise_identical():
+    """Race canary (compute-sanitizer is closed on this pool): the same matvec
+    repeated, and under every sweep tiling variant, must agree bit for bit --
+    a data race or an order-dependent reduction would show up here first."""
+    import ctypes as C
+
+    g = golden("star_l3")
+    prob = _problem(g)
+    ref = matvec_hobi(prob, g["u"])
+    for _ in range(10):
+        assert np.array_equal(matvec_hobi(prob, g["u"]), ref)
+    lib = N.load()
+    n = C.c_int(0)
+    lib.hobi_sweep_variant(prob.handle, -1, C.byref(n), None, 0)
+    for v in range(n.value):
+        N.check(lib.hobi_sweep_variant(prob.handle, v, None, None, 0))
+        assert np.array_equal(matvec_hobi(prob, g["u"]), ref), v
