@@ -122,6 +122,10 @@ int hobi_export_caches(hobi_ctx* ctx, double* reg_pos, double* reg_nrm, double* 
                        double* duf_pos, double* duf_nrm, double* duf_w, int64_t* pair_vertex,
                        int64_t* pair_face, int64_t* pair_gverts, int64_t* pair_starts);
 
+/* The rotation-0 curved element of every face, (nf, 10, 3) node positions and
+ * unit node normals: DiscretizedProblem.elements (solver.py:208-215). */
+int hobi_export_nodes(hobi_ctx* ctx, double* node_pos, double* node_nrm);
+
 /* K1..K4 of kernels.kernel_values_d (kernels.py:99-130) on the device, for n
  * displacement/normal triples (n,3); k has shape (4, n).  Test hook. */
 int hobi_kernel_values(int device, const double* d, const double* nx, const double* ny, int64_t n,

@@ -8,7 +8,9 @@ C ABI: ``include/hobi.h``.
 from .mesh import (ChargeSystem, FlatMesh, MeshFormatError, MeshValidationError, flat_area,
                    icosahedral_sphere, parse_charges, parse_msms, radial_project, write_msms)
 from .physics import FOUR_PI, KCAL_MOL_PER_E2_ANG, PhysicalParams, SingularityError
+from .kirkwood import SphereProblem, kirkwood_centered, kirkwood_series
 from .quadrature import TriangleRule, duffy_rule, gauss_radau_rule
+from .report import RunReport, ScalingRow
 from .solver import (
     DegenerateArcError,
     DiscretizedProblem,
@@ -40,4 +42,5 @@ __all__ = [
     "gauss_radau_rule", "gmres_solve", "icosahedral_sphere", "make_operator", "matvec_hobi",
     "matvec_lobi", "partition_targets", "solvation_energy", "solve", "surface_potential_error",
     "flat_area", "parse_charges", "parse_msms", "radial_project", "write_msms",
+    "SphereProblem", "kirkwood_centered", "kirkwood_series", "RunReport", "ScalingRow",
 ]

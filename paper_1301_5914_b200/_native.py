@@ -48,6 +48,7 @@ SIGNATURES = {
                                            C.c_int, C.c_int, _dp, C.POINTER(C.c_int), _dp, _dp,
                                            C.POINTER(C.c_int)]),
     "hobi_export_caches": (C.c_int, [_ctxp, _dp, _dp, _dp, _dp, _dp, _dp, _i64p, _i64p, _i64p, _i64p]),
+    "hobi_export_nodes": (C.c_int, [_ctxp, _dp, _dp]),
     "hobi_kernel_values": (C.c_int, [C.c_int, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_double,
                                      C.c_double, _dp]),
     "hobi_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),

@@ -511,6 +511,16 @@ int hobi_export_caches(hobi_ctx* c, double* reg_pos, double* reg_nrm, double* re
   return 0;
 }
 
+int hobi_export_nodes(hobi_ctx* c, double* node_pos, double* node_nrm) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (c->scheme != kHobi) return fail(HOBI_ERR_VALUE, "curved nodes exist only for scheme 'hobi'");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  if (node_pos) HOBI_CUDA(cudaMemcpy(node_pos, c->node0_pos.p, 30 * c->nf * sizeof(double), cudaMemcpyDeviceToHost));
+  if (node_nrm) HOBI_CUDA(cudaMemcpy(node_nrm, c->node0_nrm.p, 30 * c->nf * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int hobi_kernel_values(int device, const double* d, const double* nx, const double* ny, int64_t n,
                        double eps1, double eps2, double kappa, double* k) {
   HOBI_CUDA(cudaSetDevice(device));

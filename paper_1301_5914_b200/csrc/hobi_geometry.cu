@@ -237,6 +237,12 @@ int build_geometry(hobi_ctx* c, const int* pair_of_slot_host, int* first_bad_slo
       npos.p, nnrm.p, nslots, 1, c->nd, perm.p, c->duf_pos.p, c->duf_nrm.p, c->duf_w.p);
   c->launches++;
   HOBI_CUDA(cudaGetLastError());
+  // keep the rotation-0 nodes (the reference's CurvedElement per face)
+  if (c->node0_pos.alloc(30 * c->nf) || c->node0_nrm.alloc(30 * c->nf)) return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemcpy2DAsync(c->node0_pos.p, 30 * sizeof(double), npos.p, 90 * sizeof(double),
+                              30 * sizeof(double), c->nf, cudaMemcpyDeviceToDevice, c->stream));
+  HOBI_CUDA(cudaMemcpy2DAsync(c->node0_nrm.p, 30 * sizeof(double), nnrm.p, 90 * sizeof(double),
+                              30 * sizeof(double), c->nf, cudaMemcpyDeviceToDevice, c->stream));
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
 }

@@ -103,6 +103,7 @@ struct hobi_ctx {
   hobi::DevBuf<int> faces;                   // (nf,3)
   hobi::DevBuf<double> reg_pos, reg_nrm, reg_w;  // (nf,nq,3),(nf,nq,3),(nf,nq)
   hobi::DevBuf<double> duf_pos, duf_nrm, duf_w;  // pair order (3nf,nd,3)...
+  hobi::DevBuf<double> node0_pos, node0_nrm;     // rotation-0 curved nodes (nf,10,3)
   hobi::DevBuf<int> pair_vertex, pair_face, pair_gverts, pair_starts;
   std::vector<int> h_pair_starts;
   hobi::DevBuf<double> reg_bary, duf_bary;   // (nq,3), (nd,3)

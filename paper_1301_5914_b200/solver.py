@@ -30,6 +30,15 @@ from .quadrature import TriangleRule, barycentric, duffy_rule, gauss_radau_rule,
 SCHEMES = ("hobi", "lobi")
 
 
+@dataclass(frozen=True)
+class CurvedElement:
+    """10-node cubic element: positions, unit normals, source vertex ids (geometry.py:212-230)."""
+
+    nodes: np.ndarray
+    node_normals: np.ndarray
+    vertex_ids: tuple
+
+
 class DegenerateArcError(ValueError):
     """An edge arc could not be fitted (geometry.py:24-25)."""
 
@@ -195,7 +204,7 @@ class DiscretizedProblem:
         return 2 * self.n_collocation
 
     def _export(self):
-        if self._cache or self.scheme != "hobi":
+        if "reg_pos" in self._cache or self.scheme != "hobi":
             return
         nf, nq, nd = self.mesh.n_faces, len(self._rule), len(self._duffy)
         out = {
@@ -210,7 +219,7 @@ class DiscretizedProblem:
             *(N.iptr(out[k]) for k in self._CACHE[6:])))
         for a in out.values():
             a.setflags(write=False)
-        self._cache = out
+        self._cache.update(out)
 
     def __getattr__(self, name):
         if name in DiscretizedProblem._CACHE:
@@ -219,6 +228,22 @@ class DiscretizedProblem:
             self._export()
             return self._cache[name]
         raise AttributeError(name)
+
+    @property
+    def elements(self):
+        """Rotation-0 curved element per face (solver.py:208-215), from the device nodes."""
+        if self.scheme != "hobi":
+            return ()
+        if "elements" not in self._cache:
+            nf = self.mesh.n_faces
+            pos, nrm = np.empty((nf, 10, 3)), np.empty((nf, 10, 3))
+            _raise(N.load().hobi_export_nodes(self.handle, N.dptr(pos), N.dptr(nrm)))
+            self._export()
+            faces = self.mesh.faces
+            self._cache["elements"] = tuple(
+                CurvedElement(nodes=pos[f], node_normals=nrm[f], vertex_ids=tuple(int(v) for v in faces[f]))
+                for f in range(nf))
+        return self._cache["elements"]
 
     def singular_faces(self, vertex: int) -> np.ndarray:
         """Faces treated singularly for this vertex, face-ordered (solver.py:150-155)."""

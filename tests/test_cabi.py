@@ -64,3 +64,17 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "hobi_oracle" not in src and "oracle/" not in src, f
+
+
+def test_public_api_covers_the_reference_surface():
+    """Every name in pbbem.__all__ (pkg/src/pbbem/__init__.py:45-73) is importable here."""
+    import paper_1301_5914_b200 as P
+
+    reference_all = [
+        "ChargeSystem", "DiscretizedProblem", "FlatMesh", "GmresNonConvergence", "PhysicalParams",
+        "RunReport", "SolverConfig", "SphereProblem", "SurfaceSolution", "assemble_rhs",
+        "convergence_order", "discretize", "gmres_solve", "icosahedral_sphere", "kirkwood_centered",
+        "kirkwood_series", "make_operator", "matvec_hobi", "matvec_lobi", "parse_charges",
+        "partition_targets", "parse_msms", "radial_project", "solvation_energy", "solve",
+        "surface_potential_error", "write_msms"]
+    assert [n for n in reference_all if not hasattr(P, n)] == []

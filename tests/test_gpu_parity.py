@@ -364,3 +364,17 @@ def test_repeated_runs_and_all_sweep_variants_bitwise_identical():
     for v in range(n.value):
         N.check(lib.hobi_sweep_variant(prob.handle, v, None, None, 0))
         assert np.array_equal(matvec_hobi(prob, g["u"]), ref), v
+
+
+def test_elements_are_the_rotation0_nodes():
+    """problem.elements (solver.py:208-215): node 0/3/8 are the face's vertices bitwise."""
+    g = golden("star_l2")
+    prob = _problem(g)
+    els = prob.elements
+    assert len(els) == prob.mesh.n_faces
+    for f in (0, 17, len(els) - 1):
+        a, b, c = g["faces"][f]
+        e = els[f]
+        assert e.vertex_ids == (a, b, c)
+        assert np.array_equal(e.nodes[[0, 3, 8]], g["vertices"][[a, b, c]])
+        assert np.abs(np.linalg.norm(e.node_normals, axis=1) - 1).max() < 1e-12
