@@ -171,18 +171,18 @@ class DiscretizedProblem:
         self._duffy = duffy
         self._cache = {}
         self.rank, self.world = rank_info
+        x = mesh.vertices[mesh.faces]
+        cr = np.cross(x[:, 1] - x[:, 0], x[:, 2] - x[:, 0])
+        two = np.linalg.norm(cr, axis=1)
+        self.area = 0.5 * two  # flat areas, both schemes (solver.py:184, 265)
         if scheme == "hobi":
             self.colloc_pos = mesh.vertices
             self.colloc_nrm = mesh.normals
             self.reg_bary = barycentric(rule.points)
             self.duf_bary = barycentric(duffy.points)
         else:
-            x = mesh.vertices[mesh.faces]
-            cr = np.cross(x[:, 1] - x[:, 0], x[:, 2] - x[:, 0])
-            two = np.linalg.norm(cr, axis=1)
             self.colloc_pos = x.mean(axis=1)
             self.colloc_nrm = cr / two[:, None]
-            self.area = 0.5 * two
             self.reg_bary = self.duf_bary = None
 
     @property
