@@ -483,7 +483,7 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
       // small problems: if the tuned tile leaves too few work items for 148
       // SMs, use 128-row tiles (same sums bitwise, more parallelism)
       const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * kVariants[vi].r) * n_groups;
-      if (!c->variant_pinned && items < 2 * 296) vi = kSmallVariant;
+      if (!c->variant_pinned && items < 8 * 296) vi = kSmallVariant;
       const SweepVariant& v = kVariants[vi];
       fn = v.fn;
       r = v.r;
