@@ -260,6 +260,12 @@ def run_ours(a):
     sweep_avg = sweep_ms.value / max(sweep_n.value, 1)
     local_pairs = float(hi - lo) * nf * nq
     achieved = local_pairs * FLOPS_PER_PAIR / (sweep_avg * 1e-3) * 1e-12
+    ngroups, nspad = C.c_int(0), C.c_int64(0)
+    N.check(lib.hobi_sweep_layout(h, C.byref(ngroups), C.byref(nspad)))
+    # per launch: source records (96 B) + this rank's targets (48 B) + the fixed
+    # per-group partial sums (2 doubles per row per group) that keep row sums
+    # independent of the split
+    algo_bytes = 96.0 * nspad.value + 48.0 * (hi - lo) + 16.0 * ngroups.value * (hi - lo)
 
     # --- e2e: host buffers (pinned) through the C ABI, copies inside ------------
     try:
@@ -326,6 +332,7 @@ def run_ours(a):
                     "ms_per_step": e2e_ms / a.steps},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                          "frac": achieved / peak.value, "traffic": traffic,
+                         "algorithmic_bytes": algo_bytes,
                          "kernel": "sweep_kernel<kScreened,FULL>", "flops_per_pair": FLOPS_PER_PAIR,
                          "avg_launch_ms": sweep_avg, "pairs_per_launch": local_pairs,
                          "peak_source": "DFMA probe in this run (hobi_probe_fp64_tflops); "

@@ -163,6 +163,10 @@ int hobi_timing(hobi_ctx* ctx, double* sweep_ms, int64_t* sweep_launches, int64_
  * current one); reports the number of variants and the active one's name. */
 int hobi_sweep_variant(hobi_ctx* ctx, int variant, int* count, char* name, int name_len);
 
+/* Sweep layout: number of fixed source groups (partial sums per row) and the
+ * padded source count -- for the algorithmic-bytes accounting of bench.py. */
+int hobi_sweep_layout(hobi_ctx* ctx, int* n_groups, int64_t* n_sources_padded);
+
 /* Regular pairs per full matvec (N_v x N_f x nq for hobi), for throughput. */
 int hobi_pairs_per_matvec(hobi_ctx* ctx, double* pairs);
 

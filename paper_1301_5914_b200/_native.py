@@ -59,6 +59,7 @@ SIGNATURES = {
     "hobi_timing_reset": (C.c_int, [_ctxp]),
     "hobi_timing": (C.c_int, [_ctxp, _dp, _i64p, _i64p]),
     "hobi_pairs_per_matvec": (C.c_int, [_ctxp, _dp]),
+    "hobi_sweep_layout": (C.c_int, [_ctxp, C.POINTER(C.c_int), _i64p]),
     "hobi_sweep_variant": (C.c_int, [_ctxp, C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_int]),
     "hobi_bench_rows": (C.c_int, [_ctxp, _dp, C.c_int64, C.c_int64, C.c_int, C.c_int, _dp]),
     "hobi_bench": (C.c_int, [_ctxp, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp]),

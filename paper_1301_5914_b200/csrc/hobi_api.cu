@@ -712,6 +712,13 @@ int hobi_bench_rows(hobi_ctx* c, const double* u, int64_t lo, int64_t hi, int st
   return rc;
 }
 
+int hobi_sweep_layout(hobi_ctx* c, int* n_groups, int64_t* n_sources_padded) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (n_groups) *n_groups = c->n_groups;
+  if (n_sources_padded) *n_sources_padded = c->ns_pad;
+  return 0;
+}
+
 int hobi_pairs_per_matvec(hobi_ctx* c, double* pairs) {
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   *pairs = (double)c->nt * (double)c->ns;
