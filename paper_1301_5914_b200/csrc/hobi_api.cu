@@ -24,13 +24,8 @@ namespace hobi {
 
 static thread_local std::string g_last_error;
 
-void set_error(int status, const std::string& msg) {
-  (void)status;
-  g_last_error = msg;
-}
-
 int fail(int status, const std::string& msg) {
-  set_error(status, msg);
+  g_last_error = msg;
   return status;
 }
 

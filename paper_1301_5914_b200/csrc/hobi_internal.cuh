@@ -28,12 +28,7 @@ constexpr int kExpTable = 1 << kExpShift;  // 2^(j/2048) table for the FP64 exp
 enum Scheme { kHobi = 0, kLobi = 1 };
 enum KernelMode { kLaplace = 0, kScreened = 1 };
 
-struct Error {
-  int status;
-  std::string msg;
-};
-
-void set_error(int status, const std::string& msg);
+// Record `msg` as this thread's last error and return `status`.
 int fail(int status, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 
