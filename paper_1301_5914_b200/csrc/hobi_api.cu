@@ -124,6 +124,9 @@ static int common_init(hobi_ctx* c, int device, double eps1, double eps2, double
   c->device = device;
   HOBI_CUDA(cudaSetDevice(device));
   HOBI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  HOBI_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  HOBI_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+  HOBI_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   HOBI_CUDA(cudaEventCreate(&c->ev0));
   HOBI_CUDA(cudaEventCreate(&c->ev1));
   Physics& p = c->phys;
@@ -147,7 +150,7 @@ static int alloc_operands(hobi_ctx* c) {
   int rcg = choose_groups(c);
   if (rcg) return rcg;
   if (c->tgt.alloc(6 * c->nt_pad) || c->src.alloc(c->ns_pad * kSrcStride) ||
-      c->part.alloc((size_t)c->n_groups * 2 * c->nt_pad) || c->ticket.alloc(1) ||
+      c->part.alloc((size_t)c->n_groups * 2 * c->nt_pad) || c->ticket.alloc(2) ||
       c->u.alloc(std::max<int64_t>(1, 2 * c->nt)) ||
       c->out.alloc(std::max<int64_t>(1, 2 * c->nt)))
     return HOBI_ERR_CUDA;
@@ -354,9 +357,13 @@ int hobi_destroy(hobi_ctx* c) {
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
-  cudaStream_t s = c->stream;
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->fork) cudaEventDestroy(c->fork);
+  if (c->join) cudaEventDestroy(c->join);
+  cudaStream_t s = c->stream, side = c->side;
   delete c;  // DevBufs free themselves
   if (s) cudaStreamDestroy(s);
+  if (side) cudaStreamDestroy(side);
   return 0;
 }
 

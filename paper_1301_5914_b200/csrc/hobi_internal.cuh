@@ -83,6 +83,8 @@ struct hobi_ctx {
   int device = 0;
   int scheme = hobi::kHobi;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;              // Duffy swap runs here, concurrent with the sweep
+  cudaEvent_t fork = nullptr, join = nullptr;
   hobi::Physics phys{};
   int64_t nv = 0, nf = 0;  // mesh sizes
   int64_t nt = 0;          // collocation points (targets)
@@ -154,6 +156,9 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc,
 int rhs_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, double* b_dev);
 int kernel_values_device(const double* d, const double* nx, const double* ny, int64_t n,
                          double eps1, double eps2, double kappa, double* k);
+
+// Duffy swap over pairs [p0, p1) on `stream` (hobi_literal.cu)
+int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1, cudaStream_t stream);
 
 // GMRES (hobi_gmres.cu)
 struct DeviceOperator {

@@ -185,9 +185,9 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
 
-int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1) {
+int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1, cudaStream_t stream) {
   if (p1 <= p0) return 0;
-  singular_kernel<<<nblk(p1 - p0, 128), 128, 0, c->stream>>>(
+  singular_kernel<<<nblk(p1 - p0, 128), 128, 0, stream>>>(
       p0, p1, c->pair_vertex.p, c->pair_face.p, c->pair_gverts.p, c->faces.p, c->vert.p, c->vnrm.p,
       c->reg_pos.p, c->reg_nrm.p, c->reg_w.p, c->reg_bary.p, c->nq, c->duf_pos.p, c->duf_nrm.p,
       c->duf_w.p, c->duf_bary.p, c->nd, u_dev, c->nt, c->phys.er, c->phys.kappa, c->corr.p);

@@ -340,13 +340,15 @@ __global__ void __launch_bounds__(kEpiRows* kEpiSlices) epilogue_p2p_kernel(
                   ((s1[4][threadIdx.x] + s1[5][threadIdx.x]) + (s1[6][threadIdx.x] + s1[7][threadIdx.x]));
     double acc2 = ((s2[0][threadIdx.x] + s2[1][threadIdx.x]) + (s2[2][threadIdx.x] + s2[3][threadIdx.x])) +
                   ((s2[4][threadIdx.x] + s2[5][threadIdx.x]) + (s2[6][threadIdx.x] + s2[7][threadIdx.x]));
-    double c1 = 0.0, c2 = 0.0;
-    for (int p = pair_starts[v]; p < pair_starts[v + 1]; ++p) {
-      c1 += corr[2 * (int64_t)p];
-      c2 += corr[2 * (int64_t)p + 1];
+    if (corr) {
+      double c1 = 0.0, c2 = 0.0;
+      for (int p = pair_starts[v]; p < pair_starts[v + 1]; ++p) {
+        c1 += corr[2 * (int64_t)p];
+        c2 += corr[2 * (int64_t)p + 1];
+      }
+      acc1 += c1;
+      acc2 += c2;
     }
-    acc1 += c1;
-    acc2 += c2;
     const double r1 = __dsub_rn(__dmul_rn(diag1, u[v]), acc1);
     const double r2 = __dsub_rn(__dmul_rn(diag2, u[nt + v]), acc2);
     const int64_t off = (int64_t)parity * 2 * nt;
@@ -469,38 +471,55 @@ static const SweepVariant kVariants[] = {
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kSmallVariant = 3;  // R1_minb8_unroll2
 
+// Sweep phase of one operator application over rows [t0, t1).  The tuned
+// wide-tile sweep runs on the main stream; concurrently, on the side stream,
+// the Duffy swap of those rows (when swap_u is given: it needs only u) and the
+// remainder rows past the last whole wide tile, with 128-row tiles.  The side
+// stream is joined before returning (in stream order).
 int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_t t1, bool full,
-                 double* part, int64_t ldp, const int2* groups, int n_groups) {
+                 double* part, int64_t ldp, const int2* groups, int n_groups,
+                 const double* swap_u = nullptr) {
   if (t1 <= t0) return 0;
   const bool self = c->scheme == kLobi && full;
-  SweepFn fn;
-  int r = kSweepR;
+  // up to two launches over disjoint row ranges: the tuned tile over whole
+  // tiles, and 128-row tiles over the remainder.  An item costs the same
+  // whether its tile is full or not, so a part-filled last wide tile would
+  // waste up to a tile's worth of time per source group (4.8% of a 4-way
+  // split of config 4); splitting it off keeps every row's sum unchanged.
+  struct Seg {
+    SweepFn fn;
+    int r;
+    int64_t a, b;
+  } seg[2];
+  int nseg = 1;
+  seg[0] = {nullptr, kSweepR, t0, t1};
   if (c->phys.mode == kScreened) {
     if (self)
-      fn = sweep_kernel<kScreened, true, true, kSweepR, 1, 2>;
+      seg[0].fn = sweep_kernel<kScreened, true, true, kSweepR, 1, 2>;
     else if (full) {
       int vi = c->sweep_variant;
       // small problems: if the tuned tile leaves too few work items for 148
       // SMs, use 128-row tiles (same sums bitwise, more parallelism)
       const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * kVariants[vi].r) * n_groups;
       if (!c->variant_pinned && items < 8 * 296) vi = kSmallVariant;
-      const SweepVariant& v = kVariants[vi];
-      fn = v.fn;
-      r = v.r;
+      seg[0].fn = kVariants[vi].fn;
+      seg[0].r = kVariants[vi].r;
+      const int64_t tile = (int64_t)kSweepThreads * seg[0].r;
+      const int64_t whole = (t1 - t0) / tile * tile;
+      if (!c->variant_pinned && seg[0].r > 1 && whole > 0 && whole < t1 - t0) {
+        seg[0].b = t0 + whole;
+        seg[1] = {kVariants[kSmallVariant].fn, kVariants[kSmallVariant].r, t0 + whole, t1};
+        nseg = 2;
+      }
     } else
-      fn = sweep_kernel<kScreened, false, false, kSweepR, 1, 2>;
+      seg[0].fn = sweep_kernel<kScreened, false, false, kSweepR, 1, 2>;
   } else {
-    fn = self ? sweep_kernel<kLaplace, true, true, kSweepR, 1, 2>
-              : (full ? sweep_kernel<kLaplace, true, false, kSweepR, 1, 2>
-                      : sweep_kernel<kLaplace, false, false, kSweepR, 1, 2>);
+    seg[0].fn = self ? sweep_kernel<kLaplace, true, true, kSweepR, 1, 2>
+                     : (full ? sweep_kernel<kLaplace, true, false, kSweepR, 1, 2>
+                             : sweep_kernel<kLaplace, false, false, kSweepR, 1, 2>);
   }
-  HOBI_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
-  int per_sm = 0, sms = 0;
-  HOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSweepThreads, kSweepSmem));
+  int sms = 0;
   HOBI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-  const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * r) * n_groups;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)std::max(per_sm, 1) * sms));
-  HOBI_CUDA(cudaMemsetAsync(c->ticket.p, 0, sizeof(unsigned), c->stream));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {  // brackets are read lazily by collect_sweep_timing: no sync here
     if (c->ev_used + 2 > c->ev_pool.size()) {
@@ -515,10 +534,35 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
     c->ev_used += 2;
     HOBI_CUDA(cudaEventRecord(e0, c->stream));
   }
-  fn<<<grid, kSweepThreads, kSweepSmem, c->stream>>>(tgt, ldt, t0, t1, c->src.p, groups, n_groups,
-                                                     part, ldp, c->ticket.p);
-  HOBI_CUDA(cudaGetLastError());
-  c->launches++;
+  const bool use_side = nseg == 2 || swap_u;
+  if (use_side) {
+    HOBI_CUDA(cudaEventRecord(c->fork, c->stream));
+    HOBI_CUDA(cudaStreamWaitEvent(c->side, c->fork, 0));
+    if (swap_u) {
+      int rc = launch_singular(c, swap_u, c->h_pair_starts[t0], c->h_pair_starts[t1], c->side);
+      if (rc) return rc;
+    }
+  }
+  for (int k = nseg - 1; k >= 0; --k) {  // remainder first, so it is queued on the side stream early
+    const Seg& sg = seg[k];
+    cudaStream_t st = k == 1 ? c->side : c->stream;
+    unsigned* ticket = k == 1 ? c->ticket.p + 1 : c->ticket.p;
+    HOBI_CUDA(cudaFuncSetAttribute(sg.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
+    int per_sm = 0;
+    HOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sg.fn, kSweepThreads, kSweepSmem));
+    const int64_t items = (int64_t)nblk(sg.b - sg.a, kSweepThreads * sg.r) * n_groups;
+    const unsigned grid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)std::max(per_sm, 1) * sms));
+    HOBI_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
+    sg.fn<<<grid, kSweepThreads, kSweepSmem, st>>>(tgt, ldt, sg.a, sg.b, c->src.p, groups, n_groups, part,
+                                                   ldp, ticket);
+    HOBI_CUDA(cudaGetLastError());
+    c->launches++;
+  }
+  if (use_side) {
+    HOBI_CUDA(cudaEventRecord(c->join, c->side));
+    HOBI_CUDA(cudaStreamWaitEvent(c->stream, c->join, 0));
+  }
   if (c->timing) {
     HOBI_CUDA(cudaEventRecord(e1, c->stream));
     if (c->ev_used >= 256 && collect_sweep_timing(c)) return HOBI_ERR_CUDA;
@@ -581,7 +625,6 @@ std::vector<int2> make_groups(int n_src_tiles, int64_t tiles8) {
 int sweep_variant_count() { return kNumVariants; }
 const char* sweep_variant_name(int v) { return (v >= 0 && v < kNumVariants) ? kVariants[v].name : ""; }
 
-int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1);  // hobi_literal.cu
 
 int prepare_targets(hobi_ctx* c) {
   const double* pos = c->scheme == kHobi ? c->vert.p : c->reg_pos.p;  // lobi: centroids
@@ -616,17 +659,13 @@ int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi,
                        double* o2) {
   if (hi <= lo) return 0;
   int rc;
+  const bool hobi = c->scheme == kHobi;
   if ((rc = update_weights(c, u_dev))) return rc;
   if ((rc = launch_sweep(c, c->tgt.p, c->nt_pad, lo, hi, true, c->part.p, c->nt_pad, c->groups.p,
-                         c->n_groups)))
+                         c->n_groups, hobi ? u_dev : nullptr)))
     return rc;
-  const double* corr = nullptr;
-  const int* starts = nullptr;
-  if (c->scheme == kHobi) {
-    if ((rc = launch_singular(c, u_dev, c->h_pair_starts[lo], c->h_pair_starts[hi]))) return rc;
-    corr = c->corr.p;
-    starts = c->pair_starts.p;
-  }
+  const double* corr = hobi ? c->corr.p : nullptr;
+  const int* starts = hobi ? c->pair_starts.p : nullptr;
   epilogue_kernel<<<nblk(hi - lo, kEpiRows), dim3(kEpiRows, kEpiSlices), 0, c->stream>>>(
       c->part.p, c->nt_pad, c->n_groups, corr, starts, u_dev, c->nt, lo, hi, c->phys.diag1,
       c->phys.diag2, o1, o2);
@@ -642,17 +681,18 @@ static int matvec_p2p(hobi_ctx* c, const double* u_dev, double* out_dev) {
   const int parity = (int)(c->comm.epoch & 1);
   const unsigned long long target = c->comm.epoch / 2 + 1;  // arrivals per rank for this parity
   int rc;
+  const bool hobi = c->scheme == kHobi;
   if (hi > lo) {
     if ((rc = update_weights(c, u_dev))) return rc;
     if ((rc = launch_sweep(c, c->tgt.p, c->nt_pad, lo, hi, true, c->part.p, c->nt_pad, c->groups.p,
-                           c->n_groups)))
+                           c->n_groups, hobi ? u_dev : nullptr)))
       return rc;
-    if ((rc = launch_singular(c, u_dev, c->h_pair_starts[lo], c->h_pair_starts[hi]))) return rc;
   }
   // an empty range still launches one block so this rank signals its arrival
   const unsigned blocks = hi > lo ? nblk(hi - lo, kEpiRows) : 1;
   epilogue_p2p_kernel<<<blocks, dim3(kEpiRows, kEpiSlices), 0, c->stream>>>(
-      c->part.p, c->nt_pad, c->n_groups, c->corr.p, c->pair_starts.p, u_dev, c->nt, lo, hi,
+      c->part.p, c->nt_pad, c->n_groups, hobi ? c->corr.p : nullptr,
+      hobi ? c->pair_starts.p : nullptr, u_dev, c->nt, lo, hi,
       c->phys.diag1, c->phys.diag2, c->p2p_peers.p, c->comm.nranks, c->comm.rank, parity,
       c->p2p_done.p);
   p2p_wait_copy_kernel<<<std::max(1u, nblk(2 * c->nt, 1024)), 256, 0, c->stream>>>(
