@@ -89,6 +89,12 @@ int comm_allgather(hobi_ctx* c) {
                      "ncclAllGather");
 }
 
+int comm_allgather_bytes(hobi_ctx* c, const void* send, void* recv, size_t bytes) {
+  auto& a = nccl::api();
+  constexpr int kUint8 = 1;  // ncclUint8
+  return nccl::check(a.all_gather(send, recv, bytes, kUint8, c->comm.nccl, c->stream), "ncclAllGather");
+}
+
 static void row_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* hi) {
   int64_t base = n / nranks, extra = n % nranks;
   *lo = rank * base + std::min<int64_t>(rank, extra);

@@ -170,7 +170,11 @@ int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
                  int* iterations, double* residual, double* best, int* matvecs,
                  int64_t* launch_counter);
 
-// comm (hobi_api.cu)
+// comm (hobi_api.cu): the operator's row gather, and a raw byte allgather
+// (`bytes` per rank, rank-major into recv) on the context stream
 int comm_allgather(hobi_ctx* c);
+int comm_allgather_bytes(hobi_ctx* c, const void* send, void* recv, size_t bytes);
+// gathered [rank][2][m] slots -> out[0:nt] ++ out[nt:2nt] (hobi_sweep.cu)
+int gather_permute(hobi_ctx* c, double* out_dev);
 
 }  // namespace hobi

@@ -142,12 +142,12 @@ __global__ void singular_kernel(int64_t p0, int64_t p1, const int* __restrict__ 
 
 // source_terms_at (kernels.py:159-178) + /eps1 (solver.py:402); one thread per
 // collocation point, charges staged through shared memory.
-__global__ void rhs_kernel(const double* __restrict__ pos, const double* __restrict__ nrm, int64_t nt,
-                           const double* __restrict__ qpos, const double* __restrict__ q, int64_t nc,
-                           double eps1, double* __restrict__ b,
+__global__ void rhs_kernel(const double* __restrict__ pos, const double* __restrict__ nrm, int64_t lo,
+                           int64_t nt, const double* __restrict__ qpos, const double* __restrict__ q,
+                           int64_t nc, double eps1, double* __restrict__ o1, double* __restrict__ o2,
                            unsigned long long* __restrict__ bad) {
   __shared__ double sq[4][256];
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // rows [lo, nt) of this launch
   const int64_t ii = i < nt ? i : nt - 1;
   const double x0 = pos[3 * ii], x1 = pos[3 * ii + 1], x2 = pos[3 * ii + 2];
   const double m0 = nrm[3 * ii], m1 = nrm[3 * ii + 1], m2 = nrm[3 * ii + 2];
@@ -176,8 +176,8 @@ __global__ void rhs_kernel(const double* __restrict__ pos, const double* __restr
     }
   }
   if (i < nt) {
-    b[i] = s1 / eps1;
-    b[nt + i] = s2 / eps1;
+    o1[i - lo] = s1 / eps1;
+    o2[i - lo] = s2 / eps1;
   }
 }
 
@@ -210,12 +210,52 @@ int rhs_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, dou
   HOBI_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c->stream));
   const double* pos = c->scheme == kHobi ? c->vert.p : c->reg_pos.p;
   const double* nrm = c->scheme == kHobi ? c->vnrm.p : c->reg_nrm.p;
-  rhs_kernel<<<nblk(nt, 256), 256, 0, c->stream>>>(pos, nrm, nt, dpos.p, dq.p, nc, c->phys.eps1,
-                                                   b_dev, bad.p);
-  c->launches++;
-  HOBI_CUDA(cudaGetLastError());
+  // Under a communicator each rank computes its own rows and the vector is
+  // gathered like an operator application (rows are bitwise those of a
+  // one-GPU run); the singularity decision is made on every rank from all
+  // ranks' first-offender keys.  An emulated split computes every rank's
+  // rows here, straight into the gather layout.
+  const bool split = c->comm.nccl && c->comm.nranks > 1;
+  const bool emul = c->comm.emulated && c->comm.nranks > 1;
+  const int64_t m = c->gather_m;
+  auto rows = [&](int64_t lo, int64_t hi, double* o1, double* o2) -> int {
+    if (hi <= lo) return 0;
+    rhs_kernel<<<nblk(hi - lo, 256), 256, 0, c->stream>>>(pos, nrm, lo, hi, dpos.p, dq.p, nc,
+                                                          c->phys.eps1, o1, o2, bad.p);
+    c->launches++;
+    HOBI_CUDA(cudaGetLastError());
+    return 0;
+  };
+  int rc;
   unsigned long long badh = 0;
-  HOBI_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(badh), cudaMemcpyDeviceToHost, c->stream));
+  if (emul) {
+    for (int r = 0; r < c->comm.nranks; ++r) {
+      const int64_t base = nt / c->comm.nranks, extra = nt % c->comm.nranks;
+      const int64_t lo = r * base + std::min<int64_t>(r, extra), hi = lo + base + (r < extra ? 1 : 0);
+      double* slot = c->gather_recv.p + (int64_t)r * 2 * m;
+      if ((rc = rows(lo, hi, slot, slot + m))) return rc;
+    }
+    if ((rc = gather_permute(c, b_dev))) return rc;
+    HOBI_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(badh), cudaMemcpyDeviceToHost, c->stream));
+  } else if (split) {
+    if ((rc = rows(c->lo, c->hi, c->gather_send.p, c->gather_send.p + m))) return rc;
+    DevBuf<unsigned long long> all;
+    if (all.alloc(c->comm.nranks)) return HOBI_ERR_CUDA;
+    if ((rc = comm_allgather_bytes(c, bad.p, all.p, sizeof(unsigned long long)))) return rc;
+    std::vector<unsigned long long> h(c->comm.nranks);
+    HOBI_CUDA(cudaMemcpyAsync(h.data(), all.p, h.size() * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, c->stream));
+    HOBI_CUDA(cudaStreamSynchronize(c->stream));
+    badh = ~0ull;
+    for (unsigned long long v : h) badh = v < badh ? v : badh;
+    if (badh == ~0ull) {
+      if ((rc = comm_allgather(c))) return rc;
+      if ((rc = gather_permute(c, b_dev))) return rc;
+    }
+  } else {
+    if ((rc = rows(0, nt, b_dev, b_dev + nt))) return rc;
+    HOBI_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(badh), cudaMemcpyDeviceToHost, c->stream));
+  }
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
   if (badh != ~0ull) {
     unsigned long long i = badh / (unsigned long long)(nc + 1), k = badh % (unsigned long long)(nc + 1);

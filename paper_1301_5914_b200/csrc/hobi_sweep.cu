@@ -410,12 +410,24 @@ __global__ void permute_kernel(const double* __restrict__ recv, int64_t m, int64
 // Energy (solver.py:608-614): per-charge group sums in fixed group order,
 // q_k * sum_k, then one block folds the charges in a fixed tree order.
 __global__ void energy_charge_kernel(const double* __restrict__ part, int64_t ldp, int n_groups,
-                                     const double* __restrict__ q, int64_t nc, double* __restrict__ v) {
-  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= nc) return;
+                                     const double* __restrict__ q, int64_t k0, int64_t k1,
+                                     double* __restrict__ v) {
+  int64_t k = k0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= k1) return;
   double s = part[k];
   for (int g = 1; g < n_groups; ++g) s += part[(2 * (int64_t)g) * ldp + k];
-  v[k] = q[k] * s;
+  v[k - k0] = q[k] * s;
+}
+
+// rank-major [r][m] slots of per-charge values -> charge order
+__global__ void permute1_kernel(const double* __restrict__ recv, int64_t m, int64_t n, int nranks,
+                                double* __restrict__ out) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int64_t base = n / nranks, extra = n % nranks, cut = extra * (base + 1);
+  int64_t r = k < cut ? k / (base + 1) : extra + (k - cut) / (base ? base : 1);
+  int64_t lo = r < extra ? r * (base + 1) : cut + (r - extra) * base;
+  out[k] = recv[r * m + (k - lo)];
 }
 
 __global__ void energy_fold_kernel(const double* __restrict__ v, int64_t nc, double* __restrict__ out) {
@@ -722,7 +734,11 @@ int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
       return rc;
     if ((rc = comm_allgather(c))) return rc;
   }
-  permute_kernel<<<nblk(c->nt, 256), 256, 0, c->stream>>>(c->gather_recv.p, m, c->nt,
+  return gather_permute(c, out_dev);
+}
+
+int gather_permute(hobi_ctx* c, double* out_dev) {
+  permute_kernel<<<nblk(c->nt, 256), 256, 0, c->stream>>>(c->gather_recv.p, c->gather_m, c->nt,
                                                            c->comm.nranks, out_dev);
   c->launches++;
   HOBI_CUDA(cudaGetLastError());
@@ -751,16 +767,40 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, 
   c->launches++;
   int rc;
   if ((rc = update_weights(c, x_dev))) return rc;
+  // Under a communicator the charges are split across ranks; the per-charge
+  // values are gathered and folded in charge order on every rank, so the
+  // energy is bitwise that of a one-GPU run.  An emulated split computes
+  // every rank's slot here.
+  const bool split = c->comm.nccl && c->comm.nranks > 1;
+  const bool emul = c->comm.emulated && c->comm.nranks > 1;
+  const int nr = (split || emul) ? c->comm.nranks : 1;
+  const int64_t mc = (nc + nr - 1) / nr;
+  DevBuf<double> v, recv;
+  if (v.alloc(nc) || recv.alloc((size_t)nr * mc)) return HOBI_ERR_CUDA;
   bool timing = c->timing;
   c->timing = false;
-  rc = launch_sweep(c, tq.p, ldc, 0, nc, false, part.p, ldc, dgroups.p, groups);
+  for (int r = 0; r < nr; ++r) {
+    if (split && r != c->comm.rank) continue;
+    const int64_t base = nc / nr, extra = nc % nr;
+    const int64_t k0 = r * base + std::min<int64_t>(r, extra), k1 = k0 + base + (r < extra ? 1 : 0);
+    if (k1 <= k0) continue;
+    if ((rc = launch_sweep(c, tq.p, ldc, k0, k1, false, part.p, ldc, dgroups.p, groups))) break;
+    double* dst = nr == 1 ? v.p : (split ? recv.p + (int64_t)c->comm.rank * mc : recv.p + (int64_t)r * mc);
+    energy_charge_kernel<<<nblk(k1 - k0, 256), 256, 0, c->stream>>>(part.p, ldc, groups, dq.p, k0, k1, dst);
+    c->launches++;
+  }
   c->timing = timing;
   if (rc) return rc;
-  DevBuf<double> v;
-  if (v.alloc(nc)) return HOBI_ERR_CUDA;
-  energy_charge_kernel<<<nblk(nc, 256), 256, 0, c->stream>>>(part.p, ldc, groups, dq.p, nc, v.p);
+  if (split) {  // each rank contributes its slot (in place inside recv)
+    if ((rc = comm_allgather_bytes(c, recv.p + (int64_t)c->comm.rank * mc, recv.p, mc * sizeof(double))))
+      return rc;
+  }
+  if (nr > 1) {
+    permute1_kernel<<<nblk(nc, 256), 256, 0, c->stream>>>(recv.p, mc, nc, nr, v.p);
+    c->launches++;
+  }
   energy_fold_kernel<<<1, 1024, 0, c->stream>>>(v.p, nc, e.p);
-  c->launches += 2;
+  c->launches++;
   HOBI_CUDA(cudaGetLastError());
   HOBI_CUDA(cudaMemcpyAsync(energy, e.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
