@@ -466,7 +466,7 @@ int hobi_gmres(hobi_ctx* c, const double* b, double tol, int restart, int max_it
   HOBI_CUDA(cudaSetDevice(c->device));
   CtxOperator op(c);
   return gmres_device(c->device, c->stream, 2 * c->nt, &op, b, tol, restart, max_it, x, iterations,
-                      residual, best, matvecs, &c->launches);
+                      residual, best, matvecs, &c->launches, &c->gmres_ws);
 }
 
 int hobi_gmres_host_operator(int device, int64_t n, hobi_apply_fn apply, void* user, const double* b,

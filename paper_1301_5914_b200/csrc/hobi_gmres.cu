@@ -125,17 +125,12 @@ __global__ void update_kernel(const double* __restrict__ V, int64_t ldv, int64_t
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-struct Workspace {
-  DevBuf<double> V, w, x, r, b, part, hcol, nrm, y;
-  int64_t ldv = 0;
-  int grid = 1;
-};
-
 }  // namespace
 
 int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op, const double* b_host,
                  double tol, int restart, int max_it, double* x_host, int* iterations,
-                 double* residual, double* best_out, int* matvecs, int64_t* launch_counter) {
+                 double* residual, double* best_out, int* matvecs, int64_t* launch_counter,
+                 GmresWorkspace* cached) {
   if (n % 2) return fail(HOBI_ERR_VALUE, "vector length must be even: (phi, dphi/dn) halves");
   if (!(tol > 0.0 && tol < 1.0)) return fail(HOBI_ERR_VALUE, "tolerance must be in (0, 1)");
   if (restart < 1) return fail(HOBI_ERR_VALUE, "restart must be >= 1");
@@ -146,17 +141,23 @@ int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
   *matvecs = 0;
   int64_t launches = 0;
   const int m = restart;
-  Workspace ws;
-  int sms = 0, occ = 0;
-  HOBI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  HOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mgs_kernel, kGT, 0));
-  ws.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(occ, 1),
-                                                         std::min<int64_t>(2 * sms, (n + 1023) / 1024)));
-  ws.ldv = ((n + 31) / 32) * 32;
-  if (ws.V.alloc((size_t)(m + 1) * ws.ldv) || ws.w.alloc(n) || ws.x.alloc(n) || ws.r.alloc(n) ||
-      ws.b.alloc(n) || ws.part.alloc(2 * ws.grid) || ws.hcol.alloc(m + 2) || ws.nrm.alloc(1) ||
-      ws.y.alloc(m))
-    return HOBI_ERR_CUDA;
+  GmresWorkspace local;
+  GmresWorkspace& ws = cached ? *cached : local;
+  if (ws.n != n || ws.m != m) {
+    int sms = 0, occ = 0;
+    HOBI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    HOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mgs_kernel, kGT, 0));
+    ws.grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(occ, 1),
+                                                           std::min<int64_t>(2 * sms, (n + 1023) / 1024)));
+    ws.ldv = ((n + 31) / 32) * 32;
+    ws.n = -1;
+    if (ws.V.alloc((size_t)(m + 1) * ws.ldv) || ws.w.alloc(n) || ws.x.alloc(n) || ws.r.alloc(n) ||
+        ws.b.alloc(n) || ws.part.alloc(2 * ws.grid) || ws.hcol.alloc(m + 2) || ws.nrm.alloc(1) ||
+        ws.y.alloc(m))
+      return HOBI_ERR_CUDA;
+    ws.n = n;
+    ws.m = m;
+  }
   HOBI_CUDA(cudaMemcpyAsync(ws.b.p, b_host, n * sizeof(double), cudaMemcpyHostToDevice, stream));
 
   auto norm_of = [&](const double* ax, double* rout, double* val) -> int {

@@ -77,6 +77,22 @@ struct Comm {
   std::vector<void*> opened;          // peer areas opened through CUDA IPC
 };
 
+// Device workspaces kept by a context across calls: cudaMalloc/cudaFree on
+// every solve showed 0.1-0.3 s stalls on the B200 hosts.
+struct GmresWorkspace {
+  DevBuf<double> V, w, x, r, b, part, hcol, nrm, y;
+  int64_t n = -1, ldv = 0;
+  int m = -1, grid = 1;
+};
+
+struct ChargeWorkspace {  // energy / RHS buffers for one charge set size
+  int64_t nc = -1;
+  DevBuf<double> q, qpos, tq, part, v, recv, e;
+  DevBuf<int2> groups;
+  DevBuf<unsigned long long> bad, bad_all;
+  int n_groups = 0;
+};
+
 }  // namespace hobi
 
 struct hobi_ctx {
@@ -131,6 +147,8 @@ struct hobi_ctx {
   bool timing = true;
   int sweep_variant = 7;  // index into the sweep tuning table (hobi_sweep.cu): R6_minb2_unroll1
   bool variant_pinned = false;  // set by hobi_sweep_variant: no small-problem switch
+  hobi::GmresWorkspace gmres_ws;
+  hobi::ChargeWorkspace charge_ws;
 };
 
 namespace hobi {
@@ -143,6 +161,7 @@ int build_geometry(hobi_ctx* c, const int* pair_of_slot, int* first_bad_slot, in
 // sweep (hobi_sweep.cu)
 int upload_exp_table();
 int collect_sweep_timing(hobi_ctx* c);
+int charge_workspace(hobi_ctx* c, int64_t nc);
 std::vector<int2> make_groups(int n_src_tiles, int64_t target_tiles_at_8);
 int sweep_variant_count();
 const char* sweep_variant_name(int v);
@@ -168,7 +187,7 @@ struct DeviceOperator {
 int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
                  const double* b_host, double tol, int restart, int max_it, double* x_host,
                  int* iterations, double* residual, double* best, int* matvecs,
-                 int64_t* launch_counter);
+                 int64_t* launch_counter, GmresWorkspace* cached = nullptr);
 
 // comm (hobi_api.cu): the operator's row gather, and a raw byte allgather
 // (`bytes` per rank, rank-major into recv) on the context stream

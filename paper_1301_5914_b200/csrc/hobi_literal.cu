@@ -202,12 +202,14 @@ int rhs_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, dou
     HOBI_CUDA(cudaMemsetAsync(b_dev, 0, 2 * nt * sizeof(double), c->stream));
     return 0;
   }
-  DevBuf<double> dq, dpos;
-  DevBuf<unsigned long long> bad;
-  if (dq.alloc(nc) || dpos.alloc(3 * nc) || bad.alloc(1)) return HOBI_ERR_CUDA;
-  HOBI_CUDA(cudaMemcpyAsync(dq.p, q, nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  HOBI_CUDA(cudaMemcpyAsync(dpos.p, qpos, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  HOBI_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c->stream));
+  int rc;
+  if ((rc = charge_workspace(c, nc))) return rc;
+  ChargeWorkspace& w = c->charge_ws;
+  double *dq = w.q.p, *dpos = w.qpos.p;
+  unsigned long long* bad = w.bad.p;
+  HOBI_CUDA(cudaMemcpyAsync(dq, q, nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  HOBI_CUDA(cudaMemcpyAsync(dpos, qpos, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  HOBI_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), c->stream));
   const double* pos = c->scheme == kHobi ? c->vert.p : c->reg_pos.p;
   const double* nrm = c->scheme == kHobi ? c->vnrm.p : c->reg_nrm.p;
   // Under a communicator each rank computes its own rows and the vector is
@@ -220,13 +222,12 @@ int rhs_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, dou
   const int64_t m = c->gather_m;
   auto rows = [&](int64_t lo, int64_t hi, double* o1, double* o2) -> int {
     if (hi <= lo) return 0;
-    rhs_kernel<<<nblk(hi - lo, 256), 256, 0, c->stream>>>(pos, nrm, lo, hi, dpos.p, dq.p, nc,
-                                                          c->phys.eps1, o1, o2, bad.p);
+    rhs_kernel<<<nblk(hi - lo, 256), 256, 0, c->stream>>>(pos, nrm, lo, hi, dpos, dq, nc,
+                                                          c->phys.eps1, o1, o2, bad);
     c->launches++;
     HOBI_CUDA(cudaGetLastError());
     return 0;
   };
-  int rc;
   unsigned long long badh = 0;
   if (emul) {
     for (int r = 0; r < c->comm.nranks; ++r) {
@@ -236,14 +237,12 @@ int rhs_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, dou
       if ((rc = rows(lo, hi, slot, slot + m))) return rc;
     }
     if ((rc = gather_permute(c, b_dev))) return rc;
-    HOBI_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(badh), cudaMemcpyDeviceToHost, c->stream));
+    HOBI_CUDA(cudaMemcpyAsync(&badh, bad, sizeof(badh), cudaMemcpyDeviceToHost, c->stream));
   } else if (split) {
     if ((rc = rows(c->lo, c->hi, c->gather_send.p, c->gather_send.p + m))) return rc;
-    DevBuf<unsigned long long> all;
-    if (all.alloc(c->comm.nranks)) return HOBI_ERR_CUDA;
-    if ((rc = comm_allgather_bytes(c, bad.p, all.p, sizeof(unsigned long long)))) return rc;
+    if ((rc = comm_allgather_bytes(c, bad, w.bad_all.p, sizeof(unsigned long long)))) return rc;
     std::vector<unsigned long long> h(c->comm.nranks);
-    HOBI_CUDA(cudaMemcpyAsync(h.data(), all.p, h.size() * sizeof(unsigned long long),
+    HOBI_CUDA(cudaMemcpyAsync(h.data(), w.bad_all.p, h.size() * sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost, c->stream));
     HOBI_CUDA(cudaStreamSynchronize(c->stream));
     badh = ~0ull;
@@ -254,7 +253,7 @@ int rhs_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, dou
     }
   } else {
     if ((rc = rows(0, nt, b_dev, b_dev + nt))) return rc;
-    HOBI_CUDA(cudaMemcpyAsync(&badh, bad.p, sizeof(badh), cudaMemcpyDeviceToHost, c->stream));
+    HOBI_CUDA(cudaMemcpyAsync(&badh, bad, sizeof(badh), cudaMemcpyDeviceToHost, c->stream));
   }
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
   if (badh != ~0ull) {

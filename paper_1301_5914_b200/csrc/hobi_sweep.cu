@@ -745,6 +745,23 @@ int gather_permute(hobi_ctx* c, double* out_dev) {
   return 0;
 }
 
+// Buffers for a charge set of size nc, kept by the context (see GmresWorkspace).
+int charge_workspace(hobi_ctx* c, int64_t nc) {
+  ChargeWorkspace& w = c->charge_ws;
+  if (w.nc == nc) return 0;
+  const int64_t ldc = ((nc + kTargetTile - 1) / kTargetTile) * kTargetTile;
+  std::vector<int2> gtab = make_groups(c->n_src_tiles, std::max<int64_t>(1, (nc + 767) / 768));
+  w.nc = -1;
+  w.n_groups = (int)gtab.size();
+  if (w.q.alloc(nc) || w.qpos.alloc(3 * nc) || w.tq.alloc(6 * ldc) || w.e.alloc(1) ||
+      w.groups.alloc(gtab.size()) || w.part.alloc((size_t)w.n_groups * 2 * ldc) || w.v.alloc(nc) ||
+      w.recv.alloc(nc + 64) || w.bad.alloc(1) || w.bad_all.alloc(1024))
+    return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemcpy(w.groups.p, gtab.data(), gtab.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  w.nc = nc;
+  return 0;
+}
+
 int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, const double* x_dev,
                   double* energy) {
   *energy = 0.0;
@@ -752,20 +769,17 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, 
   // charges act as targets of a K1/K2-only sweep over the regular points
   // (solver.py:609-613); their "normal" is unused.
   const int64_t ldc = ((nc + kTargetTile - 1) / kTargetTile) * kTargetTile;
-  DevBuf<double> dq, dqpos, tq, part, e;
-  if (dq.alloc(nc) || dqpos.alloc(3 * nc) || tq.alloc(6 * ldc) || e.alloc(1)) return HOBI_ERR_CUDA;
-  std::vector<int2> gtab = make_groups(c->n_src_tiles, std::max<int64_t>(1, (nc + 767) / 768));
-  const int groups = (int)gtab.size();
-  DevBuf<int2> dgroups;
-  if (dgroups.alloc(groups)) return HOBI_ERR_CUDA;
-  HOBI_CUDA(cudaMemcpyAsync(dgroups.p, gtab.data(), groups * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
-  if (part.alloc((size_t)groups * 2 * ldc)) return HOBI_ERR_CUDA;
-  HOBI_CUDA(cudaMemcpyAsync(dq.p, q, nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  HOBI_CUDA(cudaMemcpyAsync(dqpos.p, qpos, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  targets_kernel<<<nblk(ldc, 256), 256, 0, c->stream>>>(dqpos.p, nullptr, nc, ldc,
-                                                        c->phys.len_scale, tq.p);
-  c->launches++;
   int rc;
+  if ((rc = charge_workspace(c, nc))) return rc;
+  ChargeWorkspace& w = c->charge_ws;
+  const int groups = w.n_groups;
+  HOBI_CUDA(cudaMemcpyAsync(w.q.p, q, nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  HOBI_CUDA(cudaMemcpyAsync(w.qpos.p, qpos, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  double *tq = w.tq.p, *part = w.part.p, *dq = w.q.p;
+  const int2* dgroups = w.groups.p;
+  targets_kernel<<<nblk(ldc, 256), 256, 0, c->stream>>>(w.qpos.p, nullptr, nc, ldc,
+                                                        c->phys.len_scale, tq);
+  c->launches++;
   if ((rc = update_weights(c, x_dev))) return rc;
   // Under a communicator the charges are split across ranks; the per-charge
   // values are gathered and folded in charge order on every rank, so the
@@ -775,8 +789,8 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, 
   const bool emul = c->comm.emulated && c->comm.nranks > 1;
   const int nr = (split || emul) ? c->comm.nranks : 1;
   const int64_t mc = (nc + nr - 1) / nr;
-  DevBuf<double> v, recv;
-  if (v.alloc(nc) || recv.alloc((size_t)nr * mc)) return HOBI_ERR_CUDA;
+  if ((size_t)nr * mc > w.recv.n && w.recv.alloc((size_t)nr * mc)) return HOBI_ERR_CUDA;
+  double *v = w.v.p, *recv = w.recv.p, *e = w.e.p;
   bool timing = c->timing;
   c->timing = false;
   for (int r = 0; r < nr; ++r) {
@@ -784,25 +798,25 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, 
     const int64_t base = nc / nr, extra = nc % nr;
     const int64_t k0 = r * base + std::min<int64_t>(r, extra), k1 = k0 + base + (r < extra ? 1 : 0);
     if (k1 <= k0) continue;
-    if ((rc = launch_sweep(c, tq.p, ldc, k0, k1, false, part.p, ldc, dgroups.p, groups))) break;
-    double* dst = nr == 1 ? v.p : (split ? recv.p + (int64_t)c->comm.rank * mc : recv.p + (int64_t)r * mc);
-    energy_charge_kernel<<<nblk(k1 - k0, 256), 256, 0, c->stream>>>(part.p, ldc, groups, dq.p, k0, k1, dst);
+    if ((rc = launch_sweep(c, tq, ldc, k0, k1, false, part, ldc, dgroups, groups))) break;
+    double* dst = nr == 1 ? v : (split ? recv + (int64_t)c->comm.rank * mc : recv + (int64_t)r * mc);
+    energy_charge_kernel<<<nblk(k1 - k0, 256), 256, 0, c->stream>>>(part, ldc, groups, dq, k0, k1, dst);
     c->launches++;
   }
   c->timing = timing;
   if (rc) return rc;
   if (split) {  // each rank contributes its slot (in place inside recv)
-    if ((rc = comm_allgather_bytes(c, recv.p + (int64_t)c->comm.rank * mc, recv.p, mc * sizeof(double))))
+    if ((rc = comm_allgather_bytes(c, recv + (int64_t)c->comm.rank * mc, recv, mc * sizeof(double))))
       return rc;
   }
   if (nr > 1) {
-    permute1_kernel<<<nblk(nc, 256), 256, 0, c->stream>>>(recv.p, mc, nc, nr, v.p);
+    permute1_kernel<<<nblk(nc, 256), 256, 0, c->stream>>>(recv, mc, nc, nr, v);
     c->launches++;
   }
-  energy_fold_kernel<<<1, 1024, 0, c->stream>>>(v.p, nc, e.p);
+  energy_fold_kernel<<<1, 1024, 0, c->stream>>>(v, nc, e);
   c->launches++;
   HOBI_CUDA(cudaGetLastError());
-  HOBI_CUDA(cudaMemcpyAsync(energy, e.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HOBI_CUDA(cudaMemcpyAsync(energy, e, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
 }
