@@ -398,3 +398,18 @@ def test_rhs_and_energy_splits_are_bitwise_identical():
         assert solvation_energy(prob, sol) == e0, ranks
         assert np.array_equal(matvec_hobi(prob, g["u"]), matvec_hobi(_problem(g), g["u"]))
     N.check(lib.hobi_emulate_ranks(prob.handle, 1))
+
+
+def test_extreme_screening_lengths_against_oracle():
+    """kappa far from the configs: tiny (coordinates scaled by kappa would
+    underflow -> Laplace instantiation) and large (exp underflow branch)."""
+    import hobi_oracle as O
+
+    g = golden("star_l2")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    u = g["u"]
+    for kap in (1e-150, 1e-9, 2.0, 50.0):
+        prob = discretize(mesh, PhysicalParams(2.0, 80.0, kap), ChargeSystem(np.zeros((0, 3)), []),
+                          SolverConfig())
+        o = O.discretize(g["vertices"], g["normals"], g["faces"], 2.0, 80.0, kap)
+        assert rel_l2(matvec_hobi(prob, u), O.matvec(o, u)) <= MATVEC_TOL, kap
