@@ -80,7 +80,7 @@ constexpr size_t kSweepSmem =
 // item's result depends only on its (tile, group), never on which CTA ran it,
 // so the sums stay deterministic.  Source tiles of every item flow through one
 // continuous kStages-deep TMA ring: `seq` counts tiles across items.
-template <int MODE, bool FULL, bool SELF, int R, int MINB, int UNROLL>
+template <int MODE, bool FULL, bool SELF, int R, int MINB, int UNROLL, bool STEP = false>
 __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
     const double* __restrict__ tgt, int64_t ldt, int64_t t_begin, int64_t t_end,
     const double* __restrict__ src, const int2* __restrict__ groups, int n_groups,
@@ -157,34 +157,39 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
       for (int j = 0; j < (warp_live ? kSrcTile : 0); ++j) {
         const double2 p01 = rec[6 * j + 0], p2m0 = rec[6 * j + 1], m12 = rec[6 * j + 2];
         double2 w01 = rec[6 * j + 3], w23 = rec[6 * j + 4], w45 = rec[6 * j + 5];
+        if constexpr (STEP) {
+          pairs_screened_stepmajor<R>(tx, ty, tz, nx, ny, nz, p01.x, p01.y, p2m0.x, p2m0.y, m12.x,
+                                      m12.y, w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, etab, a1, a2);
+        } else {
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-          double sx = p01.x, sy = p01.y, sz = p2m0.x;
-          if (SELF) {
-            // LOBI self pair: displacement forced to (1,0,0) and weights to 0, so
-            // it contributes exactly +0 (solver.py:303-310).
-            const bool self = ((int64_t)(tile0 + it) * kSrcTile + j) == tb + q;
-            if (self) {
-              sx = tx[q] - 1.0;
-              sy = ty[q];
-              sz = tz[q];
-              w01 = make_double2(0.0, 0.0);
-              w23 = w01;
-              w45 = w01;
+          for (int q = 0; q < R; ++q) {
+            double sx = p01.x, sy = p01.y, sz = p2m0.x;
+            if (SELF) {
+              // LOBI self pair: displacement forced to (1,0,0) and weights to 0, so
+              // it contributes exactly +0 (solver.py:303-310).
+              const bool self = ((int64_t)(tile0 + it) * kSrcTile + j) == tb + q;
+              if (self) {
+                sx = tx[q] - 1.0;
+                sy = ty[q];
+                sz = tz[q];
+                w01 = make_double2(0.0, 0.0);
+                w23 = w01;
+                w45 = w01;
+              }
+            }
+            if (MODE == kScreened)
+              pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, p2m0.y, m12.x,
+                                  m12.y, w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, etab, a1[q], a2[q]);
+            else
+              pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, p2m0.y, m12.x,
+                                 m12.y, w23.x, w45.x, a1[q], a2[q]);
+            if (SELF) {
+              w01 = rec[6 * j + 3];
+              w23 = rec[6 * j + 4];
+              w45 = rec[6 * j + 5];
             }
           }
-          if (MODE == kScreened)
-            pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, p2m0.y, m12.x,
-                                m12.y, w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, etab, a1[q], a2[q]);
-          else
-            pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, p2m0.y, m12.x,
-                               m12.y, w23.x, w45.x, a1[q], a2[q]);
-          if (SELF) {
-            w01 = rec[6 * j + 3];
-            w23 = rec[6 * j + 4];
-            w45 = rec[6 * j + 5];
-          }
-        }
+        }  // STEP
       }
       __syncthreads();
     }
@@ -474,12 +479,16 @@ struct SweepVariant {
 // targets per thread x min CTAs per SM (register cap) x source unroll.
 #define HOBI_V(R, M, U) \
   { sweep_kernel<kScreened, true, false, R, M, U>, R, "R" #R "_minb" #M "_unroll" #U }
+#define HOBI_VS(R, M, U) \
+  { sweep_kernel<kScreened, true, false, R, M, U, true>, R, "step_R" #R "_minb" #M "_unroll" #U }
 static const SweepVariant kVariants[] = {
     HOBI_V(2, 1, 2), HOBI_V(2, 6, 2), HOBI_V(4, 3, 2), HOBI_V(1, 8, 2), HOBI_V(4, 3, 1),
     HOBI_V(4, 4, 1), HOBI_V(3, 4, 1), HOBI_V(6, 2, 1), HOBI_V(8, 2, 1), HOBI_V(3, 4, 2),
-    HOBI_V(4, 4, 2), HOBI_V(5, 3, 1),
+    HOBI_V(4, 4, 2), HOBI_V(5, 3, 1), HOBI_VS(6, 2, 1), HOBI_VS(4, 3, 1), HOBI_VS(3, 4, 1),
+    HOBI_VS(4, 3, 2),
 };
 #undef HOBI_V
+#undef HOBI_VS
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kSmallVariant = 3;  // R1_minb8_unroll2
 
