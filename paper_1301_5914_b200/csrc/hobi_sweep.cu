@@ -9,12 +9,13 @@
 //   tgt  : SoA (6, nt_pad)  x', y', z', nx, ny, nz   (x' = len_scale * x)
 //   src  : AoS (ns_pad, 12) x', y', z', nx, ny, nz, W1, A, B, C, D, W4
 //   part : (n_groups, 2, nt_pad) per-source-group partial sums
-// A CTA owns kTargetTile targets (kSweepR per thread, in registers) and one
-// fixed source group; source tiles of kSrcTile records stream through a
+// The sweep is persistent: each resident CTA pulls work items (a tile of
+// 128*R targets held R per thread in registers, x one fixed source group)
+// from an atomic ticket; source tiles of kSrcTile records stream through a
 // kStages-deep shared-memory ring filled by the TMA bulk-copy engine
 // (cp.async.bulk + mbarrier).  Source groups depend only on the problem, never
-// on the row split, so every row's sum is bitwise identical for any number of
-// GPUs (solver.py:12-17).
+// on the row split or the tiling, so every row's sum is bitwise identical for
+// any number of GPUs (solver.py:12-17).
 #include <algorithm>
 #include <cmath>
 
