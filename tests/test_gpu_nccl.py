@@ -3,7 +3,6 @@ runs the same send slot -> ncclAllGather -> permutation kernel sequence as an
 8-way split does, and must reproduce the plain operator bitwise."""
 
 import ctypes as C
-import os
 
 import numpy as np
 import pytest

@@ -1,5 +1,5 @@
 """Scratch: reproduce bench.py's sequence and trace the GMRES solve timing."""
-import sys, time, ctypes as C
+import sys, time
 import numpy as np
 sys.path.insert(0, '.')
 from paper_1301_5914_b200 import _native as N, discretize, PhysicalParams, SolverConfig, assemble_rhs, make_operator, gmres_solve, solvation_energy

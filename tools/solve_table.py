@@ -1,6 +1,5 @@
 """Solve-time table for BASELINE configs 1..5 on one GPU, with a breakdown."""
 import sys, time, json, ctypes as C
-import numpy as np
 sys.path.insert(0, '.')
 from paper_1301_5914_b200 import (_native as N, discretize, PhysicalParams, SolverConfig, assemble_rhs,
                                   make_operator, gmres_solve, solvation_energy)
