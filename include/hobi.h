@@ -61,6 +61,21 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
                 const double* duf_pts, const double* duf_wts, const double* duf_shape, int nd,
                 hobi_ctx** out);
 
+/*
+ * Build a HOBI context from caches computed elsewhere -- e.g. the fields of
+ * the reference's own DiscretizedProblem (solver.py:122-140: reg_pos/nrm/w,
+ * reg_bary, duf_pos/nrm/w, duf_bary, pair_vertex/face/gverts/starts, in the
+ * reference's layouts) -- so a pbbem installation can keep its discretize
+ * and swap in only the operator, GMRES, RHS and energy.
+ */
+int hobi_create_from_caches(int device, const double* vertices, const double* normals, int64_t nv,
+                            const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
+                            const double* reg_pos, const double* reg_nrm, const double* reg_w,
+                            const double* reg_bary, int nq, const double* duf_pos,
+                            const double* duf_nrm, const double* duf_w, const double* duf_bary, int nd,
+                            const int64_t* pair_vertex, const int64_t* pair_face,
+                            const int64_t* pair_gverts, const int64_t* pair_starts, hobi_ctx** out);
+
 /* LOBI (flat centroid) discretisation: solver.py:177-186.  No rules needed. */
 int hobi_create_lobi(int device, const double* vertices, const double* normals, int64_t nv,
                      const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,

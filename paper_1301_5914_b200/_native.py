@@ -33,6 +33,10 @@ SIGNATURES = {
     "hobi_create": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _i64p, C.c_int64, C.c_double, C.c_double,
                               C.c_double, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp, C.c_int,
                               C.POINTER(_ctxp)]),
+    "hobi_create_from_caches": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _i64p, C.c_int64, C.c_double,
+                                          C.c_double, C.c_double, _dp, _dp, _dp, _dp, C.c_int, _dp,
+                                          _dp, _dp, _dp, C.c_int, _i64p, _i64p, _i64p, _i64p,
+                                          C.POINTER(_ctxp)]),
     "hobi_create_lobi": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _i64p, C.c_int64, C.c_double,
                                    C.c_double, C.c_double, C.POINTER(_ctxp)]),
     "hobi_destroy": (C.c_int, [_ctxp]),

@@ -309,6 +309,80 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
   return 0;
 }
 
+int hobi_create_from_caches(int device, const double* vertices, const double* normals, int64_t nv,
+                            const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
+                            const double* reg_pos, const double* reg_nrm, const double* reg_w,
+                            const double* reg_bary, int nq, const double* duf_pos,
+                            const double* duf_nrm, const double* duf_w, const double* duf_bary, int nd,
+                            const int64_t* pair_vertex, const int64_t* pair_face,
+                            const int64_t* pair_gverts, const int64_t* pair_starts, hobi_ctx** out) {
+  *out = nullptr;
+  if (nq < 1 || nq > 16 || nd < 1 || nd > 64) return fail(HOBI_ERR_VALUE, "rule sizes out of range");
+  if (nv < 1 || nf < 1) return fail(HOBI_ERR_VALUE, "mesh must have vertices and faces");
+  if (nv >= (1ll << 31) || 3 * nf >= (1ll << 31)) return fail(HOBI_ERR_VALUE, "mesh too large");
+  const int64_t np = 3 * nf;
+  if (pair_starts[0] != 0 || pair_starts[nv] != np)
+    return fail(HOBI_ERR_VALUE, "pair_starts must run from 0 to 3*n_faces");
+  for (int64_t i = 0; i < 3 * nf; ++i)
+    if (faces[i] < 0 || faces[i] >= nv) return fail(HOBI_ERR_VALUE, "face index out of range");
+  hobi_ctx* c = new hobi_ctx();
+  auto bail = [&](int r) {
+    hobi_destroy(c);
+    return r;
+  };
+  int rc;
+  if ((rc = common_init(c, device, eps1, eps2, kappa))) return bail(rc);
+  if ((rc = check_extent(c, vertices, nv))) return bail(rc);
+  c->scheme = kHobi;
+  c->nv = nv;
+  c->nf = nf;
+  c->nt = nv;
+  c->nq = nq;
+  c->nd = nd;
+  c->ns = nf * nq;
+  auto narrow = [](const int64_t* a, int64_t n) {
+    std::vector<int> v(n);
+    for (int64_t i = 0; i < n; ++i) v[i] = (int)a[i];
+    return v;
+  };
+  std::vector<int> f32 = narrow(faces, 3 * nf), pv = narrow(pair_vertex, np), pf = narrow(pair_face, np),
+                   pg = narrow(pair_gverts, 3 * np), ps = narrow(pair_starts, nv + 1);
+  c->h_pair_starts = ps;
+  if (c->vert.alloc(3 * nv) || c->vnrm.alloc(3 * nv) || c->faces.alloc(3 * nf) ||
+      c->reg_pos.alloc(3 * nf * nq) || c->reg_nrm.alloc(3 * nf * nq) || c->reg_w.alloc(nf * nq) ||
+      c->duf_pos.alloc(3 * np * nd) || c->duf_nrm.alloc(3 * np * nd) || c->duf_w.alloc(np * nd) ||
+      c->pair_vertex.alloc(np) || c->pair_face.alloc(np) || c->pair_gverts.alloc(3 * np) ||
+      c->pair_starts.alloc(nv + 1) || c->reg_bary.alloc(3 * nq) || c->duf_bary.alloc(3 * nd) ||
+      c->corr.alloc(2 * np))
+    return bail(HOBI_ERR_CUDA);
+  struct Up {
+    void* d;
+    const void* h;
+    size_t bytes;
+  } ups[] = {{c->vert.p, vertices, 3 * nv * sizeof(double)},
+             {c->vnrm.p, normals, 3 * nv * sizeof(double)},
+             {c->faces.p, f32.data(), 3 * nf * sizeof(int)},
+             {c->reg_pos.p, reg_pos, 3 * nf * nq * sizeof(double)},
+             {c->reg_nrm.p, reg_nrm, 3 * nf * nq * sizeof(double)},
+             {c->reg_w.p, reg_w, nf * nq * sizeof(double)},
+             {c->reg_bary.p, reg_bary, 3 * nq * sizeof(double)},
+             {c->duf_pos.p, duf_pos, 3 * np * nd * sizeof(double)},
+             {c->duf_nrm.p, duf_nrm, 3 * np * nd * sizeof(double)},
+             {c->duf_w.p, duf_w, np * nd * sizeof(double)},
+             {c->duf_bary.p, duf_bary, 3 * nd * sizeof(double)},
+             {c->pair_vertex.p, pv.data(), np * sizeof(int)},
+             {c->pair_face.p, pf.data(), np * sizeof(int)},
+             {c->pair_gverts.p, pg.data(), 3 * np * sizeof(int)},
+             {c->pair_starts.p, ps.data(), (nv + 1) * sizeof(int)}};
+  for (const Up& u : ups) {
+    cudaError_t e = cudaMemcpy(u.d, u.h, u.bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMemcpy(upload caches)"));
+  }
+  if ((rc = alloc_operands(c))) return bail(rc);
+  *out = c;
+  return 0;
+}
+
 int hobi_create_lobi(int device, const double* vertices, const double* normals, int64_t nv,
                      const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
                      hobi_ctx** out) {
@@ -529,6 +603,8 @@ int hobi_export_caches(hobi_ctx* c, double* reg_pos, double* reg_nrm, double* re
 int hobi_export_nodes(hobi_ctx* c, double* node_pos, double* node_nrm) {
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   if (c->scheme != kHobi) return fail(HOBI_ERR_VALUE, "curved nodes exist only for scheme 'hobi'");
+  if (!c->node0_pos.p)
+    return fail(HOBI_ERR_STATE, "curved nodes are not kept for a context built from caches");
   HOBI_CUDA(cudaSetDevice(c->device));
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
   if (node_pos) HOBI_CUDA(cudaMemcpy(node_pos, c->node0_pos.p, 30 * c->nf * sizeof(double), cudaMemcpyDeviceToHost));

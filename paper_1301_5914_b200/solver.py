@@ -288,6 +288,56 @@ def discretize(mesh: FlatMesh, params: PhysicalParams, charges: ChargeSystem,
     return DiscretizedProblem(mesh, params, charges, config.scheme, handle, rule, duffy, (rank, world))
 
 
+def problem_from_caches(reference_problem, config: SolverConfig | None = None) -> DiscretizedProblem:
+    """Device problem from an already discretised reference problem.
+
+    ``reference_problem`` is any object with the fields of the reference's
+    DiscretizedProblem (solver.py:119-140: mesh, params, charges, reg_pos,
+    reg_nrm, reg_w, reg_bary, duf_pos, duf_nrm, duf_w, duf_bary, pair_vertex,
+    pair_face, pair_gverts, pair_starts) -- e.g. pbbem's own.  The caches are
+    uploaded as they are (no device geometry), so an installation can keep its
+    discretize and run only the operator, RHS, GMRES and energy here.
+    """
+    rp = reference_problem
+    if getattr(rp, "scheme", "hobi") != "hobi":
+        raise ValueError("caches exist only for scheme 'hobi'")
+    N.require_device()
+    config = config or SolverConfig()
+    m = rp.mesh
+    v, n, f = N.f64(m.vertices), N.f64(m.normals), N.i64(m.faces)
+    arr = {k: N.f64(getattr(rp, k)) for k in ("reg_pos", "reg_nrm", "reg_w", "reg_bary", "duf_pos",
+                                               "duf_nrm", "duf_w", "duf_bary")}
+    ints = {k: N.i64(getattr(rp, k)) for k in ("pair_vertex", "pair_face", "pair_gverts", "pair_starts")}
+    nq, nd = arr["reg_w"].shape[1], arr["duf_w"].shape[1]
+    ctx = C.c_void_p()
+    p = rp.params
+    _raise(N.load().hobi_create_from_caches(
+        _device_index(), N.dptr(v), N.dptr(n), m.n_vertices, N.iptr(f), m.n_faces, p.eps1, p.eps2,
+        p.kappa, N.dptr(arr["reg_pos"]), N.dptr(arr["reg_nrm"]), N.dptr(arr["reg_w"]),
+        N.dptr(arr["reg_bary"]), nq, N.dptr(arr["duf_pos"]), N.dptr(arr["duf_nrm"]),
+        N.dptr(arr["duf_w"]), N.dptr(arr["duf_bary"]), nd, N.iptr(ints["pair_vertex"]),
+        N.iptr(ints["pair_face"]), N.iptr(ints["pair_gverts"]), N.iptr(ints["pair_starts"]),
+        C.byref(ctx)))
+    handle = _Handle(ctx.value)
+    rank, world, _ = _world()
+    if world > 1:
+        from .distributed import init_nccl_comm
+
+        init_nccl_comm(handle.ptr, rank, world)
+    mesh = FlatMesh(m.vertices, m.normals, m.faces)
+    charges = ChargeSystem(rp.charges.positions, rp.charges.charges)
+    prob = DiscretizedProblem(mesh, p, charges, "hobi", handle, _rule_of(arr["reg_bary"]),
+                              _rule_of(arr["duf_bary"]), (rank, world))
+    prob.reg_bary, prob.duf_bary = arr["reg_bary"], arr["duf_bary"]
+    return prob
+
+
+def _rule_of(bary):
+    """A stand-in rule with the uploaded points (sizes and bookkeeping only)."""
+    pts = np.clip(np.asarray(bary)[:, 1:3], 0.0, 1.0)
+    return TriangleRule(pts, np.full(len(pts), 0.5 / len(pts)), "uploaded", 0)
+
+
 def _as_vector(problem, u):
     u = N.f64(u)
     T = problem.n_collocation
@@ -490,6 +540,6 @@ def convergence_order(coarse_mesh: float, fine_mesh: float, coarse_error: float,
 __all__ = [
     "DegenerateArcError", "DiscretizedProblem", "GmresNonConvergence", "GpuOperator", "SCHEMES",
     "SolverConfig", "SurfaceSolution", "apply_rows", "assemble_rhs", "convergence_order",
-    "discretize", "gmres_solve", "make_operator", "matvec_hobi", "matvec_lobi", "partition_targets",
+    "discretize", "gmres_solve", "make_operator", "problem_from_caches", "matvec_hobi", "matvec_lobi", "partition_targets",
     "solvation_energy", "solve", "surface_potential_error", "FOUR_PI", "KCAL_MOL_PER_E2_ANG",
 ]

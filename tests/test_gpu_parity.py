@@ -413,3 +413,29 @@ def test_extreme_screening_lengths_against_oracle():
                           SolverConfig())
         o = O.discretize(g["vertices"], g["normals"], g["faces"], 2.0, 80.0, kap)
         assert rel_l2(matvec_hobi(prob, u), O.matvec(o, u)) <= MATVEC_TOL, kap
+
+
+def test_problem_from_reference_caches():
+    """The reference's own DiscretizedProblem caches (golden fields) uploaded as
+    they are: the operator equals the device-geometry operator bit for bit
+    (the caches are bitwise the same) and the reference's A u."""
+    from types import SimpleNamespace
+
+    from paper_1301_5914_b200.solver import problem_from_caches
+
+    g = golden("star_l2")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    ref = SimpleNamespace(mesh=mesh, params=PhysicalParams(*g["params"]),
+                          charges=ChargeSystem(g["qpos"], g["q"]), scheme="hobi",
+                          **{k: g[k] for k in ("reg_pos", "reg_nrm", "reg_w", "reg_bary", "duf_pos",
+                                               "duf_nrm", "duf_w", "duf_bary", "pair_vertex",
+                                               "pair_face", "pair_gverts", "pair_starts")})
+    up = problem_from_caches(ref)
+    assert np.array_equal(matvec_hobi(up, g["u"]), matvec_hobi(_problem(g), g["u"]))
+    assert rel_l2(matvec_hobi(up, g["u"]), g["Au"]) <= MATVEC_TOL
+    assert rel_l2(assemble_rhs(up), g["rhs"]) <= 1e-14
+    cfg = SolverConfig(workers=1, restart=int(g["restart"]))
+    with make_operator(up, cfg) as op:
+        sol = gmres_solve(op, assemble_rhs(up), cfg)
+    assert sol.iterations == int(g["iterations"])
+    assert abs(solvation_energy(up, sol) - float(g["energy"])) <= SOLVE_TOL * abs(float(g["energy"]))
