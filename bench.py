@@ -301,6 +301,25 @@ def run_ours(a):
                  "residual": sol.residual, "energy_kcal_mol": energy,
                  "includes": "rhs + GMRES(restart %d, tol %g) + energy, wall clock" % (cfg.restart, cfg.tol)}
 
+    # one-GPU model of the p-way row split: the slowest of the first and last
+    # rank's compute (everything before the gather), device-timed; labelled a
+    # model -- the real multi-GPU numbers come from torchrun runs of this file
+    split_model = None
+    if world == 1:
+        split_model = {"what": "slowest-rank compute of a p-way split timed on this GPU (no collective)"}
+        t1 = None
+        for p in (1, 2, 4, 8):
+            worst = 0.0
+            for r in ((0,) if p == 1 else (0, p - 1)):
+                base, extra = divmod(nv, p)
+                rlo = r * base + min(r, extra)
+                rhi = rlo + base + (1 if r < extra else 0)
+                msr = np.zeros(3)
+                N.check(lib.hobi_bench_rows(h, N.dptr(u), rlo, rhi, 3, 1, N.dptr(msr)))
+                worst = max(worst, float(np.median(msr)))
+            t1 = worst if p == 1 else t1
+            split_model[str(p)] = {"rank_ms": worst, "efficiency": t1 / (p * worst)}
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         s = _cpu_sample(cfg, u, a.cpu_rows)
@@ -340,6 +359,7 @@ def run_ours(a):
             "gpu_launches": int(launches.value),
             "clocks": clocks.summary(),
             "solve": solve,
+            "split_model": split_model,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
