@@ -219,6 +219,7 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
                 const double* reg_pts, const double* reg_wts, const double* reg_shape, int nq,
                 const double* duf_pts, const double* duf_wts, const double* duf_shape, int nd,
                 hobi_ctx** out) {
+  NvtxRange nvtx_("hobi_create");
   *out = nullptr;
   if (nq < 1 || nq > 16) return fail(HOBI_ERR_VALUE, "regular rule must have 1..16 points");
   if (nd < 1 || nd > 64) return fail(HOBI_ERR_VALUE, "Duffy rule must have 1..64 points");
@@ -462,12 +463,14 @@ int hobi_size(hobi_ctx* c, int64_t* n_colloc, int64_t* n_sources) {
 }
 
 int hobi_matvec_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
+  NvtxRange nvtx_("hobi_matvec_device");
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   HOBI_CUDA(cudaSetDevice(c->device));
   return matvec_full_device(c, u_dev, out_dev);
 }
 
 int hobi_matvec(hobi_ctx* c, const double* u, double* out) {
+  NvtxRange nvtx_("hobi_matvec");
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   HOBI_CUDA(cudaSetDevice(c->device));
   const size_t bytes = 2 * c->nt * sizeof(double);
@@ -496,6 +499,7 @@ int hobi_matvec_rows(hobi_ctx* c, const double* u, int64_t lo, int64_t hi, doubl
 }
 
 int hobi_rhs(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, double* b) {
+  NvtxRange nvtx_("hobi_rhs");
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   HOBI_CUDA(cudaSetDevice(c->device));
   int rc = rhs_device(c, qpos, q, nc, c->out.p);
@@ -507,6 +511,7 @@ int hobi_rhs(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, doubl
 
 int hobi_energy(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, const double* phi,
                 const double* dphi, double* energy) {
+  NvtxRange nvtx_("hobi_energy");
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   HOBI_CUDA(cudaSetDevice(c->device));
   HOBI_CUDA(cudaMemcpyAsync(c->u.p, phi, c->nt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -543,6 +548,7 @@ struct HostOperator : DeviceOperator {
 
 int hobi_gmres(hobi_ctx* c, const double* b, double tol, int restart, int max_it, double* x,
                int* iterations, double* residual, double* best, int* matvecs) {
+  NvtxRange nvtx_("hobi_gmres");
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   HOBI_CUDA(cudaSetDevice(c->device));
   CtxOperator op(c);

@@ -7,9 +7,17 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/hobi.h"
 
 namespace hobi {
+
+// NVTX range for timeline tools (header-only NVTX v3; a no-op without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr double kFourPi = 12.566370614359172;  // 4.0 * np.pi (kernels.py:27)
 constexpr double kKcal = 332.0716;               // kernels.py:33
