@@ -207,6 +207,46 @@ def variants_case():
     case("star_l2_lobi", star.surface(2), few, 2.0, 80.0, 0.1257, solve=True, restart=20, scheme="lobi")
 
 
+def uv_sphere(n_lat, n_lon, radius):
+    """Latitude-longitude sphere: pole vertices of valence n_lon, skinny polar
+    triangles -- a mesh family unlike the icospheres (valence 5/6)."""
+    verts = [(0.0, 0.0, 1.0)]
+    for i in range(1, n_lat):
+        th = np.pi * i / n_lat
+        for j in range(n_lon):
+            ph = 2 * np.pi * j / n_lon + (0.5 * np.pi / n_lon if i % 2 else 0.0)
+            verts.append((np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th)))
+    verts.append((0.0, 0.0, -1.0))
+    verts = np.asarray(verts)
+    ring = lambda i, j: 1 + (i - 1) * n_lon + (j % n_lon)  # noqa: E731
+    faces = [(0, ring(1, j), ring(1, j + 1)) for j in range(n_lon)]
+    for i in range(1, n_lat - 1):
+        for j in range(n_lon):
+            a, b, c, d = ring(i, j), ring(i, j + 1), ring(i + 1, j), ring(i + 1, j + 1)
+            faces += [(a, c, d), (a, d, b)]
+    south = len(verts) - 1
+    faces += [(south, ring(n_lat - 1, j + 1), ring(n_lat - 1, j)) for j in range(n_lon)]
+    faces = np.asarray(faces, dtype=np.int64)
+    x = verts[faces]
+    geo = np.cross(x[:, 1] - x[:, 0], x[:, 2] - x[:, 0])
+    flip = np.einsum("ij,ij->i", geo, x.mean(axis=1)) < 0
+    faces[flip] = faces[flip][:, ::-1]
+    from paper_1301_5914_b200.mesh import FlatMesh
+
+    return FlatMesh(vertices=radius * verts, normals=verts, faces=faces)
+
+
+def uv_case():
+    mesh = uv_sphere(10, 16, 2.0)
+    rng = np.random.default_rng(21)
+    pos = rng.uniform(-0.8, 0.8, size=(6, 3))
+    from paper_1301_5914_b200.mesh import ChargeSystem
+
+    charges = ChargeSystem(positions=pos, charges=rng.choice([-1.0, 1.0], 6))
+    case("uv_sphere", mesh, charges, 2.0, 80.0, 0.3, restart=15, caches=True, solve=True,
+         kirkwood_radius=2.0)
+
+
 def main():
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -215,6 +255,7 @@ def main():
     msms_case()
     kirkwood_case()
     variants_case()
+    uv_case()
     kernel_table()
     degenerate_case()
     star = StarShape.from_seed(16.0, seed=3)

@@ -77,7 +77,7 @@ def test_kernel_values_match_reference():
             assert np.all(err[nz] <= bound[i][nz]), (tag, i, (err[nz] / bound[i][nz]).max())
 
 
-@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2"])
+@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "uv_sphere"])
 def test_geometry_caches_bit_exact(name):
     g = golden(name)
     prob = _problem(g)
@@ -89,7 +89,7 @@ def test_geometry_caches_bit_exact(name):
         assert np.array_equal(getattr(prob, key), g[key]), key
 
 
-@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "star_l3", "c1", "c2"])
+@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "star_l3", "c1", "c2", "uv_sphere"])
 def test_matvec_matches_reference(name):
     g = golden(name)
     prob = _problem(g)
@@ -97,14 +97,14 @@ def test_matvec_matches_reference(name):
     assert rel_l2(got, g["Au"]) <= MATVEC_TOL
 
 
-@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "star_l3", "c1", "c2"])
+@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "star_l3", "c1", "c2", "uv_sphere"])
 def test_rhs_matches_reference(name):
     g = golden(name)
     prob = _problem(g)
     assert rel_l2(assemble_rhs(prob), g["rhs"]) <= 1e-14
 
 
-@pytest.mark.parametrize("name", ["star_l2", "star_l3", "c1", "c2"])
+@pytest.mark.parametrize("name", ["star_l2", "star_l3", "c1", "c2", "uv_sphere"])
 def test_solve_matches_reference(name):
     g = golden(name)
     prob = _problem(g, restart=int(g["restart"]))

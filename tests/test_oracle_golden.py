@@ -20,7 +20,7 @@ def _disc(g, scheme="hobi", charges=True):
     return O.discretize(g["vertices"], g["normals"], g["faces"], e1, e2, k, scheme=scheme)
 
 
-@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2"])
+@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "uv_sphere"])
 def test_oracle_caches_bit_exact(name):
     g = golden(name)
     p = _disc(g)
@@ -30,7 +30,7 @@ def test_oracle_caches_bit_exact(name):
         assert np.array_equal(getattr(p, key), g[key]), key
 
 
-@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "star_l3", "c1", "c2"])
+@pytest.mark.parametrize("name", ["sphere_l1_mixed", "star_l2", "star_l3", "c1", "c2", "uv_sphere"])
 def test_oracle_matvec_and_rhs(name):
     g = golden(name)
     p = _disc(g)
@@ -38,7 +38,7 @@ def test_oracle_matvec_and_rhs(name):
     assert rel_l2(O.rhs(p), g["rhs"]) <= 1e-15
 
 
-@pytest.mark.parametrize("name", ["star_l2", "c1"])
+@pytest.mark.parametrize("name", ["star_l2", "c1", "uv_sphere"])
 def test_oracle_solve_and_energy(name):
     g = golden(name)
     p = _disc(g)
