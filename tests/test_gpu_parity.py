@@ -439,3 +439,29 @@ def test_problem_from_reference_caches():
         sol = gmres_solve(op, assemble_rhs(up), cfg)
     assert sol.iterations == int(g["iterations"])
     assert abs(solvation_energy(up, sol) - float(g["energy"])) <= SOLVE_TOL * abs(float(g["energy"]))
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13, 14])
+def test_random_surfaces_against_oracle(seed):
+    """Seeded random star surfaces / parameters / vectors: device caches are
+    bitwise the oracle's (which is bitwise the reference's), matvec and RHS to
+    1e-12, LOBI too."""
+    import hobi_oracle as O
+    from paper_1301_5914_b200.surfaces import StarShape
+
+    rng = np.random.default_rng(seed)
+    shape = StarShape.from_seed(float(rng.uniform(5, 40)), seed=seed, amplitude=float(rng.uniform(0.05, 0.2)))
+    mesh = shape.surface(int(rng.integers(1, 4)))
+    charges = shape.interior_charges(int(rng.integers(1, 40)), seed=seed + 100)
+    e1, e2, kap = float(rng.uniform(1, 8)), float(rng.uniform(2, 90)), float(rng.choice([0.0, rng.uniform(0.01, 1.0)]))
+    prob = discretize(mesh, PhysicalParams(e1, e2, kap), charges, SolverConfig())
+    o = O.discretize(mesh.vertices, mesh.normals, mesh.faces, e1, e2, kap, charges.positions, charges.charges)
+    for key in ("reg_pos", "reg_nrm", "reg_w", "duf_pos", "duf_nrm", "duf_w"):
+        assert np.array_equal(getattr(prob, key), getattr(o, key)), key
+    u = rng.standard_normal(prob.n_unknowns)
+    assert rel_l2(matvec_hobi(prob, u), O.matvec(o, u)) <= MATVEC_TOL
+    assert rel_l2(assemble_rhs(prob), O.rhs(o)) <= 1e-13
+    pl = discretize(mesh, PhysicalParams(e1, e2, kap), charges, SolverConfig(scheme="lobi"))
+    ol = O.discretize(mesh.vertices, mesh.normals, mesh.faces, e1, e2, kap, scheme="lobi")
+    ul = rng.standard_normal(pl.n_unknowns)
+    assert rel_l2(matvec_lobi(pl, ul), O.matvec(ol, ul)) <= MATVEC_TOL
