@@ -227,9 +227,10 @@ def test_born_sphere_frozen_energy():
     assert solvation_energy(prob, sol) == pytest.approx(-86.3199784371863, rel=1e-9)
 
 
-@pytest.mark.parametrize("index", [3, 4])
+@pytest.mark.parametrize("index", [3, 4, 5])
 def test_large_config_rows_vs_oracle(index):
-    """Configs 3-4 at full size: sampled rows against the oracle's _apply_range."""
+    """Configs 3-5 at full size (config 5: 327,680 triangles, 2.1e11 pairs per
+    matvec): sampled rows against the oracle's _apply_range."""
     import hobi_oracle as O
     from paper_1301_5914_b200.surfaces import baseline_config
 
