@@ -262,10 +262,10 @@ def run_ours(a):
     achieved = local_pairs * FLOPS_PER_PAIR / (sweep_avg * 1e-3) * 1e-12
     ngroups, nspad = C.c_int(0), C.c_int64(0)
     N.check(lib.hobi_sweep_layout(h, C.byref(ngroups), C.byref(nspad)))
-    # per launch: source records (96 B) + this rank's targets (48 B) + the fixed
+    # per launch: source records (80 B) + this rank's targets (48 B) + the fixed
     # per-group partial sums (2 doubles per row per group) that keep row sums
     # independent of the split
-    algo_bytes = 96.0 * nspad.value + 48.0 * (hi - lo) + 16.0 * ngroups.value * (hi - lo)
+    algo_bytes = 80.0 * nspad.value + 48.0 * (hi - lo) + 16.0 * ngroups.value * (hi - lo)
 
     # --- e2e: host buffers (pinned) through the C ABI, copies inside ------------
     try:

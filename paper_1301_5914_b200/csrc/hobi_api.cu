@@ -182,10 +182,11 @@ static int check_extent(hobi_ctx* c, const double* v, int64_t n) {
   for (int k = 0; k < 3; ++k) diag += (hi[k] - lo[k]) * (hi[k] - lo[k]);
   if (c->phys.kappa * std::sqrt(diag) > 1e9)
     return fail(HOBI_ERR_VALUE, "kappa * mesh extent exceeds the supported range (1e9)");
-  if (c->phys.kappa * std::sqrt(diag) < 1e-100) {
-    // screening below 1e-100 of the geometry changes no kernel value at double
-    // precision, and kappa-scaled coordinates would underflow: use the kappa = 0
-    // instantiation (K1 = K4 = 0) for the sweep
+  if (c->phys.kappa * std::sqrt(diag) < 1e-30) {
+    // screening this weak changes every kernel value by a relative O(kappa r)
+    // <= 1e-30, far below double rounding, while kappa-scaled coordinates and
+    // the k^3-weighted source normals would head for underflow: use the
+    // kappa = 0 instantiation (K1 = K4 = 0) for the sweep
     c->phys.mode = kLaplace;
     c->phys.len_scale = 1.0;
   }

@@ -1,9 +1,10 @@
 // FP64 pair arithmetic of the all-pairs sweep, hand-scheduled
 // for the B200 FP64 pipe.  See DESIGN.md "kernel algebra" for the derivation:
 // coordinates are pre-scaled by kappa so r' = kappa*r, the physical constants
-// (1/4pi, kappa^n, er, 1/er) are folded into six per-source weights, expm1 and
-// exp share one table-driven range reduction, and 1/r comes from the MUFU
-// rsqrt seed plus one third-order Newton step.  48 FP64 instructions per pair
+// (1/4pi, kappa^n, er, 1/er) are folded into the per-source record (the wp
+// weight rides on the source normal) and two launch constants, expm1 and exp
+// share one table-driven range reduction, and 1/r comes from the MUFU rsqrt
+// seed plus one third-order Newton step.  45 FP64 instructions per pair
 // (vs ~95 for a literal libdevice transcription of kernels.py:112-130).
 #pragma once
 
@@ -47,39 +48,41 @@ __device__ __forceinline__ double expm1_neg(double x, const double* __restrict__
   return fma(S, p, S - 1.0);
 }
 
-// Screened pair (kappa > 0), scaled coordinates.  Source weights:
-//   W1 = -k wd/4pi, A = k^2 er wp/4pi, B = k^2 (er-1) wp/4pi,
-//   C = k^2 wd/(4pi er), D = -k^2 (1-1/er) wd/4pi, W4 = k^3 wp/4pi.
+// Screened pair (kappa > 0), scaled coordinates.  Source record:
+//   m' = M m with M = k^3 wp/4pi (the source normal carries the wp weight),
+//   W1 = -k wd/4pi, C = k^2 wd/(4pi er), D = -k^2 (1-1/er) wd/4pi,
+// and two launch constants Ap = er/k, Bp = (er-1)/k (so M (a Ap + Bp) =
+// k^2 wp (a er + er - 1)/4pi).  With dny' = d.m' = M dny, u = dny'/r^2:
+//   K1 wd + K2 wp = (1/r) (W1 em1 + u (a Ap + Bp))
+//   K3 wd + K4 wp = (1/r^3) (dnx (t2 - u b) + a nn')
+// where t2 = a C + D, b = 3a + kr*kre (kernels.py:119-120), nn' = n.m'.
 // acc1 += K1 wd + K2 wp ; acc2 += K3 wd + K4 wp   (solver.py:333-334)
+// 45 FP64 instructions per pair (25 DFMA, 14 DMUL, 6 DADD).
 template <bool FULL>
 __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, double nx, double ny,
                                               double nz, double sx, double sy, double sz, double mx,
-                                              double my, double mz, double W1, double A, double B,
-                                              double C, double D, double W4,
-                                              const double* __restrict__ etab, double& acc1,
-                                              double& acc2) {
+                                              double my, double mz, double W1, double C, double D,
+                                              double Ap, double Bp, const double* __restrict__ etab,
+                                              double& acc1, double& acc2) {
   double dx = tx - sx, dy = ty - sy, dz = tz - sz;
   double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   double dny = fma(dx, mx, fma(dy, my, dz * mz));
   double ir = rsqrt_fast(r2);
   double r = r2 * ir;  // kappa * |x - y|
   double ir2 = ir * ir;
-  double ir3 = ir2 * ir;
   double em1 = expm1_neg(r, etab);
   double kre = fma(r, em1, r);  // kr e^{-kr}
   double a = em1 + kre;         // (1+kr)e^{-kr} - 1      (kernels.py:119)
-  acc1 = fma(em1 * ir, W1, acc1);                 // K1 wd
-  acc1 = fma(dny * ir3, fma(a, A, B), acc1);      // K2 wp
+  double u = dny * ir2;
+  double t = fma(a, Ap, Bp);
+  acc1 = fma(ir, fma(em1, W1, u * t), acc1);
   if (FULL) {
     double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
     double nn = fma(nx, mx, fma(ny, my, nz * mz));
-    // K3 wd + K4 wp = ir3 (dnx (a C + D) + W4 (a P - z)), with b = 3a + kr*kre
-    // (kernels.py:120) folded as a nn - b Q = a (nn - 3Q) - kr kre Q, Q = dnx dny / r^2
-    double Q = (dnx * dny) * ir2;
-    double P = fma(Q, -3.0, nn);
-    double z = (r * kre) * Q;
-    double k4 = W4 * fma(a, P, -z);
-    acc2 = fma(ir3, fma(dnx, fma(a, C, D), k4), acc2);
+    double b = fma(a, 3.0, r * kre);  // kernels.py:120
+    double g = fma(-u, b, fma(a, C, D));
+    double X = fma(dnx, g, a * nn);
+    acc2 = fma(ir, X * ir2, acc2);
   }
 }
 
@@ -92,9 +95,9 @@ template <int R>
 __device__ __forceinline__ void pairs_screened_stepmajor(
     const double (&tx)[R], const double (&ty)[R], const double (&tz)[R], const double (&nx)[R],
     const double (&ny)[R], const double (&nz)[R], double sx, double sy, double sz, double mx, double my,
-    double mz, double W1, double A, double B, double C, double D, double W4,
-    const double* __restrict__ etab, double (&acc1)[R], double (&acc2)[R]) {
-  double dx[R], dy[R], dz[R], r2[R], dny[R], dnx[R], nn[R], ir[R], r[R], em1[R], a[R];
+    double mz, double W1, double C, double D, double Ap, double Bp, const double* __restrict__ etab,
+    double (&acc1)[R], double (&acc2)[R]) {
+  double dx[R], dy[R], dz[R], r2[R], dny[R], dnx[R], nn[R], ir[R], r[R], em1[R], a[R], kre[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) dx[q] = tx[q] - sx;
 #pragma unroll
@@ -124,53 +127,54 @@ __device__ __forceinline__ void pairs_screened_stepmajor(
   }
 #pragma unroll
   for (int q = 0; q < R; ++q) em1[q] = expm1_neg(r[q], etab);
-  double kre[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     kre[q] = fma(r[q], em1[q], r[q]);
     a[q] = em1[q] + kre[q];
   }
-#pragma unroll
-  for (int q = 0; q < R; ++q) acc1[q] = fma(em1[q] * ir[q], W1, acc1[q]);
-  double t[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) t[q] = fma(a[q], A, B);
-  double ir2[R], ir3[R];
+  double ir2[R], u[R], t[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     ir2[q] = ir[q] * ir[q];
-    ir3[q] = ir2[q] * ir[q];
-    acc1[q] = fma(dny[q] * ir3[q], t[q], acc1[q]);
+    u[q] = dny[q] * ir2[q];
   }
+#pragma unroll
+  for (int q = 0; q < R; ++q) t[q] = fma(a[q], Ap, Bp);
+#pragma unroll
+  for (int q = 0; q < R; ++q) t[q] = u[q] * t[q];
+#pragma unroll
+  for (int q = 0; q < R; ++q) t[q] = fma(em1[q], W1, t[q]);
+#pragma unroll
+  for (int q = 0; q < R; ++q) acc1[q] = fma(ir[q], t[q], acc1[q]);
 #pragma unroll
   for (int q = 0; q < R; ++q) t[q] = fma(a[q], C, D);
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    const double Q = (dnx[q] * dny[q]) * ir2[q];
-    const double P = fma(Q, -3.0, nn[q]);
-    const double z = (r[q] * kre[q]) * Q;
-    const double v = fma(a[q], P, -z);
-    dny[q] = v;  // reuse storage
+    const double b = fma(a[q], 3.0, r[q] * kre[q]);
+    t[q] = fma(-u[q], b, t[q]);
   }
 #pragma unroll
-  for (int q = 0; q < R; ++q) dny[q] = W4 * dny[q];
+  for (int q = 0; q < R; ++q) nn[q] = a[q] * nn[q];
 #pragma unroll
-  for (int q = 0; q < R; ++q) acc2[q] = fma(ir3[q], fma(dnx[q], t[q], dny[q]), acc2[q]);
+  for (int q = 0; q < R; ++q) {
+    const double X = fma(dnx[q], t[q], nn[q]);
+    acc2[q] = fma(ir[q], X * ir2[q], acc2[q]);
+  }
 }
 
 // Unscreened pair (kappa == 0): K1 = K4 = 0 exactly, as in the reference
-// (expm1(0) = 0 makes a = b = 0).  Weights B = (er-1) wp/4pi, D = -(1-1/er) wd/4pi.
+// (expm1(0) = 0 makes a = b = 0).  Record: m' = (er-1) wp/4pi m, D = -(1-1/er) wd/4pi.
 template <bool FULL>
 __device__ __forceinline__ void pair_laplace(double tx, double ty, double tz, double nx, double ny,
                                              double nz, double sx, double sy, double sz, double mx,
-                                             double my, double mz, double B, double D,
-                                             double& acc1, double& acc2) {
+                                             double my, double mz, double D, double& acc1,
+                                             double& acc2) {
   double dx = tx - sx, dy = ty - sy, dz = tz - sz;
   double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   double dny = fma(dx, mx, fma(dy, my, dz * mz));
   double ir = rsqrt_fast(r2);
   double ir3 = (ir * ir) * ir;
-  acc1 = fma(dny * ir3, B, acc1);
+  acc1 = fma(dny, ir3, acc1);
   if (FULL) {
     double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
     acc2 = fma(dnx * ir3, D, acc2);

@@ -27,7 +27,7 @@ constexpr int kSweepThreads = 128;  // threads per CTA
 constexpr int kSweepR = 2;          // targets held in registers per thread
 constexpr int kTargetTile = kSweepThreads * kSweepR;
 constexpr int kSrcTile = 64;        // sources per shared-memory stage
-constexpr int kSrcStride = 12;      // doubles per source record
+constexpr int kSrcStride = 10;      // doubles per source record
 constexpr int kStages = 4;          // TMA bulk-copy pipeline depth
 constexpr int kMaxRanks = 64;      // P2P gather: arrival counters per buffer parity
 constexpr int kExpShift = 11;

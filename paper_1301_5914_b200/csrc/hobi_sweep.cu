@@ -7,7 +7,8 @@
 //
 // Layout in HBM:
 //   tgt  : SoA (6, nt_pad)  x', y', z', nx, ny, nz   (x' = len_scale * x)
-//   src  : AoS (ns_pad, 12) x', y', z', nx, ny, nz, W1, A, B, C, D, W4
+//   src  : AoS (ns_pad, 10) x', y', z', M nx, M ny, M nz, W1, C, D, 0
+//          (M = k^3 wp/4pi screened, (er-1) wp/4pi unscreened; hobi_fastmath.cuh)
 //   part : (n_groups, 2, nt_pad) per-source-group partial sums
 // The sweep is persistent: each resident CTA pulls work items (a tile of
 // 128*R targets held R per thread in registers, x one fixed source group)
@@ -85,7 +86,7 @@ template <int MODE, bool FULL, bool SELF, int R, int MINB, int UNROLL, bool STEP
 __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
     const double* __restrict__ tgt, int64_t ldt, int64_t t_begin, int64_t t_end,
     const double* __restrict__ src, const int2* __restrict__ groups, int n_groups,
-    double* __restrict__ part, int64_t ldp, unsigned* __restrict__ ticket) {
+    double* __restrict__ part, int64_t ldp, unsigned* __restrict__ ticket, double Ap, double Bp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
   double* etab = ring + kStages * kSrcTile * kSrcStride;
@@ -156,39 +157,34 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
       const double2* rec = reinterpret_cast<const double2*>(ring + st * kSrcTile * kSrcStride);
 #pragma unroll UNROLL
       for (int j = 0; j < (warp_live ? kSrcTile : 0); ++j) {
-        const double2 p01 = rec[6 * j + 0], p2m0 = rec[6 * j + 1], m12 = rec[6 * j + 2];
-        double2 w01 = rec[6 * j + 3], w23 = rec[6 * j + 4], w45 = rec[6 * j + 5];
+        const double2 p01 = rec[5 * j + 0], p2m0 = rec[5 * j + 1], m12 = rec[5 * j + 2];
+        const double2 w01 = rec[5 * j + 3], w2x = rec[5 * j + 4];
         if constexpr (STEP) {
           pairs_screened_stepmajor<R>(tx, ty, tz, nx, ny, nz, p01.x, p01.y, p2m0.x, p2m0.y, m12.x,
-                                      m12.y, w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, etab, a1, a2);
+                                      m12.y, w01.x, w01.y, w2x.x, Ap, Bp, etab, a1, a2);
         } else {
 #pragma unroll
           for (int q = 0; q < R; ++q) {
             double sx = p01.x, sy = p01.y, sz = p2m0.x;
+            double mx = p2m0.y, my = m12.x, mz = m12.y, W1 = w01.x, C = w01.y, D = w2x.x;
             if (SELF) {
-              // LOBI self pair: displacement forced to (1,0,0) and weights to 0, so
-              // it contributes exactly +0 (solver.py:303-310).
+              // LOBI self pair: displacement forced to (1,0,0) and every weight
+              // (the weighted normal included) to 0, so it contributes exactly +0
+              // (solver.py:303-310).
               const bool self = ((int64_t)(tile0 + it) * kSrcTile + j) == tb + q;
               if (self) {
                 sx = tx[q] - 1.0;
                 sy = ty[q];
                 sz = tz[q];
-                w01 = make_double2(0.0, 0.0);
-                w23 = w01;
-                w45 = w01;
+                mx = my = mz = W1 = C = D = 0.0;
               }
             }
             if (MODE == kScreened)
-              pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, p2m0.y, m12.x,
-                                  m12.y, w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, etab, a1[q], a2[q]);
+              pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, mx, my, mz, W1,
+                                  C, D, Ap, Bp, etab, a1[q], a2[q]);
             else
-              pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, p2m0.y, m12.x,
-                                 m12.y, w23.x, w45.x, a1[q], a2[q]);
-            if (SELF) {
-              w01 = rec[6 * j + 3];
-              w23 = rec[6 * j + 4];
-              w45 = rec[6 * j + 5];
-            }
+              pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, mx, my, mz, D,
+                                 a1[q], a2[q]);
           }
         }  // STEP
       }
@@ -206,10 +202,10 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
   }
 }
 
-// Scaled static source geometry: record fields 0..5.
-__global__ void static_sources_kernel(const double* __restrict__ pos, const double* __restrict__ nrm,
-                                      int64_t ns, int64_t ns_pad, double scale,
-                                      double* __restrict__ src) {
+// Scaled static source positions: record fields 0..2; padding records get
+// zero weights (fields 3..9), so they contribute exactly +-0.
+__global__ void static_sources_kernel(const double* __restrict__ pos, int64_t ns, int64_t ns_pad,
+                                      double scale, double* __restrict__ src) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= ns_pad) return;
   double* rec = src + s * kSrcStride;
@@ -217,18 +213,12 @@ __global__ void static_sources_kernel(const double* __restrict__ pos, const doub
     rec[0] = scale * pos[3 * s];
     rec[1] = scale * pos[3 * s + 1];
     rec[2] = scale * pos[3 * s + 2];
-    rec[3] = nrm[3 * s];
-    rec[4] = nrm[3 * s + 1];
-    rec[5] = nrm[3 * s + 2];
-  } else {  // padding: far away, unit normal, zero weights -> contributes +-0 exactly
+  } else {  // padding: far away
     rec[0] = 1e6 + (double)(s - ns);
     rec[1] = 1e6;
     rec[2] = 1e6;
-    rec[3] = 1.0;
-    rec[4] = 0.0;
-    rec[5] = 0.0;
   }
-  for (int k = 6; k < 12; ++k) rec[k] = 0.0;
+  for (int k = 3; k < kSrcStride; ++k) rec[k] = 0.0;
 }
 
 // Targets SoA, scaled.
@@ -245,14 +235,16 @@ __global__ void targets_kernel(const double* __restrict__ pos, const double* __r
   tgt[5 * ldt + t] = nrm ? nrm[3 * i + 2] : 0.0;
 }
 
-// K-C: interpolate u onto the regular points and fold the physics into the six
-// per-source weights.  phi_q = v0 b0 + v1 b1 + v2 b2 (solver.py:269-275),
-// wphi = reg_w * phi_q (solver.py:321-322).
+// K-C: interpolate u onto the regular points and fold the physics into the
+// per-source record.  phi_q = v0 b0 + v1 b1 + v2 b2 (solver.py:269-275),
+// wphi = reg_w * phi_q (solver.py:321-322); the wp-weighted terms ride on the
+// source normal (fields 3..5), the wd-weighted ones are W1, C, D.
 __global__ void source_weights_kernel(const double* __restrict__ u, int64_t nt,
                                       const int* __restrict__ faces, const double* __restrict__ reg_w,
                                       const double* __restrict__ bary, int nq, int64_t ns,
-                                      const double* __restrict__ area, double kA, double kB, double kC,
-                                      double kD, double kW1, double kW4, double* __restrict__ src) {
+                                      const double* __restrict__ area, const double* __restrict__ nrm,
+                                      double kM, double kW1, double kC, double kD,
+                                      double* __restrict__ src) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= ns) return;
   double wp, wd;
@@ -272,12 +264,14 @@ __global__ void source_weights_kernel(const double* __restrict__ u, int64_t nt,
     wd = w * dp;
   }
   double* rec = src + s * kSrcStride;
+  const double M = kM * wp;
+  rec[3] = M * nrm[3 * s];
+  rec[4] = M * nrm[3 * s + 1];
+  rec[5] = M * nrm[3 * s + 2];
   rec[6] = kW1 * wd;
-  rec[7] = kA * wp;
-  rec[8] = kB * wp;
-  rec[9] = kC * wd;
-  rec[10] = kD * wd;
-  rec[11] = kW4 * wp;
+  rec[7] = kC * wd;
+  rec[8] = kD * wd;
+  rec[9] = 0.0;
 }
 
 // K-D: fixed-order group reduction + Duffy swap (solver.py:362-363) + diagonal
@@ -468,7 +462,7 @@ int collect_sweep_timing(hobi_ctx* c) {
 namespace {
 
 typedef void (*SweepFn)(const double*, int64_t, int64_t, int64_t, const double*, const int2*, int,
-                        double*, int64_t, unsigned*);
+                        double*, int64_t, unsigned*, double, double);
 
 struct SweepVariant {
   SweepFn fn;
@@ -492,6 +486,28 @@ static const SweepVariant kVariants[] = {
 #undef HOBI_VS
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kSmallVariant = 3;  // R1_minb8_unroll2
+
+// Physics folded into the per-source record and the launch constants Ap, Bp
+// (see hobi_fastmath.cuh).
+struct WeightConstants {
+  double kM, kW1, kC, kD, Ap, Bp;
+};
+WeightConstants weight_constants(const Physics& p) {
+  WeightConstants w{};
+  if (p.mode == kScreened) {
+    const double k = p.kappa, k2 = k * k / kFourPi;
+    w.kM = k * k2;  // k^3/4pi
+    w.kW1 = -k / kFourPi;
+    w.kC = k2 / p.er;
+    w.kD = -k2 * (1.0 - 1.0 / p.er);
+    w.Ap = p.er / k;
+    w.Bp = (p.er - 1.0) / k;
+  } else {
+    w.kM = (p.er - 1.0) / kFourPi;
+    w.kD = -(1.0 - 1.0 / p.er) / kFourPi;
+  }
+  return w;
+}
 
 // Sweep phase of one operator application over rows [t0, t1).  The tuned
 // wide-tile sweep runs on the main stream; concurrently, on the side stream,
@@ -542,6 +558,7 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
   }
   int sms = 0;
   HOBI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  const WeightConstants wc = weight_constants(c->phys);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {  // brackets are read lazily by collect_sweep_timing: no sync here
     if (c->ev_used + 2 > c->ev_pool.size()) {
@@ -577,7 +594,7 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)std::max(per_sm, 1) * sms));
     HOBI_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
     sg.fn<<<grid, kSweepThreads, kSweepSmem, st>>>(tgt, ldt, sg.a, sg.b, c->src.p, groups, n_groups, part,
-                                                   ldp, ticket);
+                                                   ldp, ticket, wc.Ap, wc.Bp);
     HOBI_CUDA(cudaGetLastError());
     c->launches++;
   }
@@ -592,18 +609,6 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
   return 0;
 }
 
-// Physics folded into the per-source weights (see hobi_fastmath.cuh).
-void weight_constants(const Physics& p, double* kA, double* kB, double* kC, double* kD, double* kW1,
-                      double* kW4) {
-  const double k = p.mode == kScreened ? p.kappa : 1.0;
-  const double k2 = k * k / kFourPi;
-  *kW1 = p.mode == kScreened ? -k / kFourPi : 0.0;
-  *kA = p.mode == kScreened ? k2 * p.er : 0.0;
-  *kB = k2 * (p.er - 1.0);
-  *kC = p.mode == kScreened ? k2 / p.er : 0.0;
-  *kD = -k2 * (1.0 - 1.0 / p.er);
-  *kW4 = p.mode == kScreened ? k * k2 : 0.0;
-}
 
 }  // namespace
 
@@ -660,18 +665,17 @@ int prepare_targets(hobi_ctx* c) {
 
 int prepare_static_sources(hobi_ctx* c) {
   static_sources_kernel<<<nblk(c->ns_pad, 256), 256, 0, c->stream>>>(
-      c->reg_pos.p, c->reg_nrm.p, c->ns, c->ns_pad, c->phys.len_scale, c->src.p);
+      c->reg_pos.p, c->ns, c->ns_pad, c->phys.len_scale, c->src.p);
   c->launches++;
   HOBI_CUDA(cudaGetLastError());
   return 0;
 }
 
 static int update_weights(hobi_ctx* c, const double* u_dev) {
-  double kA, kB, kC, kD, kW1, kW4;
-  weight_constants(c->phys, &kA, &kB, &kC, &kD, &kW1, &kW4);
+  const WeightConstants w = weight_constants(c->phys);
   source_weights_kernel<<<nblk(c->ns, 256), 256, 0, c->stream>>>(
       u_dev, c->nt, c->faces.p, c->reg_w.p, c->reg_bary.p, c->nq, c->ns,
-      c->scheme == kLobi ? c->lobi_area.p : nullptr, kA, kB, kC, kD, kW1, kW4, c->src.p);
+      c->scheme == kLobi ? c->lobi_area.p : nullptr, c->reg_nrm.p, w.kM, w.kW1, w.kC, w.kD, c->src.p);
   c->launches++;
   HOBI_CUDA(cudaGetLastError());
   return 0;

@@ -409,7 +409,7 @@ def test_extreme_screening_lengths_against_oracle():
     g = golden("star_l2")
     mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
     u = g["u"]
-    for kap in (1e-150, 1e-9, 2.0, 50.0):
+    for kap in (1e-150, 1e-35, 1e-25, 1e-9, 2.0, 50.0):
         prob = discretize(mesh, PhysicalParams(2.0, 80.0, kap), ChargeSystem(np.zeros((0, 3)), []),
                           SolverConfig())
         o = O.discretize(g["vertices"], g["normals"], g["faces"], 2.0, 80.0, kap)
