@@ -161,7 +161,10 @@ int hobi_comm_init(hobi_ctx* ctx, const unsigned char id[128], int nranks, int r
  * peer memory) and signals arrival with system-scope atomics; a wait kernel
  * hands the gathered vector on.  After hobi_comm_init, every rank calls
  * hobi_comm_p2p_handle, the host all-gathers the 64-byte handles (rank
- * order), and every rank calls hobi_comm_p2p_open with all of them.
+ * order), and every rank calls hobi_comm_p2p_open with all of them.  If a
+ * peer's rows do not arrive within HOBI_P2P_TIMEOUT_MS (environment, default
+ * 60000, read at open) the wait gives up and the next synchronising call
+ * returns HOBI_ERR_NCCL; the context's P2P gather is unusable afterwards.
  */
 int hobi_comm_p2p_handle(hobi_ctx* ctx, unsigned char handle[64]);
 int hobi_comm_p2p_open(hobi_ctx* ctx, const unsigned char* handles, int nranks, int rank);

@@ -443,6 +443,7 @@ int hobi_destroy(hobi_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->comm.opened) cudaIpcCloseMemHandle(p);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->p2p_err) cudaFreeHost(c->p2p_err);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -481,7 +482,7 @@ int hobi_matvec(hobi_ctx* c, const double* u, double* out) {
   if (rc) return rc;
   HOBI_CUDA(cudaMemcpyAsync(out, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
-  return 0;
+  return p2p_check(c);
 }
 
 int hobi_matvec_rows(hobi_ctx* c, const double* u, int64_t lo, int64_t hi, double* o1, double* o2) {
@@ -525,7 +526,10 @@ namespace {
 struct CtxOperator : DeviceOperator {
   hobi_ctx* c;
   explicit CtxOperator(hobi_ctx* ctx) : c(ctx) {}
-  int apply(const double* in, double* out) override { return matvec_full_device(c, in, out); }
+  int apply(const double* in, double* out) override {
+    int rc = p2p_check(c);  // GMRES has synchronised on the previous application
+    return rc ? rc : matvec_full_device(c, in, out);
+  }
 };
 
 struct HostOperator : DeviceOperator {
@@ -553,8 +557,10 @@ int hobi_gmres(hobi_ctx* c, const double* b, double tol, int restart, int max_it
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   HOBI_CUDA(cudaSetDevice(c->device));
   CtxOperator op(c);
-  return gmres_device(c->device, c->stream, 2 * c->nt, &op, b, tol, restart, max_it, x, iterations,
-                      residual, best, matvecs, &c->launches, &c->gmres_ws);
+  int rc = gmres_device(c->device, c->stream, 2 * c->nt, &op, b, tol, restart, max_it, x, iterations,
+                        residual, best, matvecs, &c->launches, &c->gmres_ws);
+  int rc2 = p2p_check(c);
+  return rc2 ? rc2 : rc;
 }
 
 int hobi_gmres_host_operator(int device, int64_t n, hobi_apply_fn apply, void* user, const double* b,
@@ -693,6 +699,16 @@ int hobi_comm_p2p_open(hobi_ctx* c, const unsigned char* handles, int nranks, in
   if (c->p2p_peers.alloc(nranks) || c->p2p_done.alloc(1)) return HOBI_ERR_CUDA;
   HOBI_CUDA(cudaMemcpy(c->p2p_peers.p, ptrs.data(), nranks * sizeof(double*), cudaMemcpyHostToDevice));
   HOBI_CUDA(cudaMemset(c->p2p_done.p, 0, sizeof(unsigned)));
+  if (!c->p2p_err) {
+    HOBI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->p2p_err), sizeof(int), cudaHostAllocMapped));
+    HOBI_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->p2p_err_dev), c->p2p_err, 0));
+  }
+  *c->p2p_err = 0;
+  const char* tmo = getenv("HOBI_P2P_TIMEOUT_MS");
+  const double ms = tmo ? atof(tmo) : 60000.0;
+  c->p2p_timeout_ns = (unsigned long long)((ms > 0 ? ms : 60000.0) * 1e6);
+  const char* extra = getenv("HOBI_P2P_TEST_MISSING_ARRIVALS");
+  c->p2p_extra = extra ? (unsigned long long)atoll(extra) : 0;
   c->comm.p2p = true;
   c->comm.epoch = 0;
   return 0;
@@ -757,6 +773,7 @@ int hobi_bench(hobi_ctx* c, const double* u, double* out, int steps, int mode, i
     float t = 0.f;
     HOBI_CUDA(cudaEventElapsedTime(&t, e0, e1));
     ms[i] = t;
+    rc = p2p_check(c);
   }
   if (!rc && mode == 0 && out) {
     HOBI_CUDA(cudaMemcpyAsync(out, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));

@@ -142,6 +142,12 @@ struct hobi_ctx {
   hobi::DevBuf<double> p2p_area;
   hobi::DevBuf<double*> p2p_peers;
   hobi::DevBuf<unsigned> p2p_done;
+  // peer-arrival watchdog: the wait kernel gives up after p2p_timeout_ns and
+  // raises *p2p_err (mapped pinned host memory), which synchronising calls check
+  int* p2p_err = nullptr;
+  int* p2p_err_dev = nullptr;
+  unsigned long long p2p_timeout_ns = 0;
+  unsigned long long p2p_extra = 0;  // test hook: wait for arrivals that never come
   int64_t gather_m = 0;
   hobi::Comm comm;
 
@@ -203,5 +209,6 @@ int comm_allgather(hobi_ctx* c);
 int comm_allgather_bytes(hobi_ctx* c, const void* send, void* recv, size_t bytes);
 // gathered [rank][2][m] slots -> out[0:nt] ++ out[nt:2nt] (hobi_sweep.cu)
 int gather_permute(hobi_ctx* c, double* out_dev);
+int p2p_check(hobi_ctx* c);
 
 }  // namespace hobi

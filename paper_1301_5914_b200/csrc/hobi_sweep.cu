@@ -377,14 +377,30 @@ __global__ void __launch_bounds__(kEpiRows* kEpiSlices) epilogue_p2p_kernel(
 
 // Wait until all ranks' rows of this epoch have arrived, then hand the
 // gathered vector to the caller's buffer.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void p2p_wait_copy_kernel(const double* __restrict__ area, int64_t nt, int nranks, int parity,
-                                     unsigned long long target, double* __restrict__ out) {
+                                     unsigned long long target, unsigned long long timeout_ns,
+                                     int* err, double* __restrict__ out) {
   if (threadIdx.x == 0) {
     volatile unsigned long long* flag =
         reinterpret_cast<volatile unsigned long long*>(const_cast<double*>(area) + 4 * nt) +
         parity * kMaxRanks;
-    for (int r = 0; r < nranks; ++r)
-      while (flag[r] < target) __nanosleep(64);
+    const unsigned long long t0 = global_ns();
+    bool late = false;
+    for (int r = 0; r < nranks && !late; ++r)
+      while (flag[r] < target) {
+        if (global_ns() - t0 > timeout_ns) {  // a peer is gone: report instead of hanging the GPU
+          *reinterpret_cast<volatile int*>(err) = 1;
+          late = true;
+          break;
+        }
+        __nanosleep(128);
+      }
     __threadfence_system();
   }
   __syncthreads();
@@ -705,7 +721,7 @@ int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi,
 static int matvec_p2p(hobi_ctx* c, const double* u_dev, double* out_dev) {
   const int64_t lo = c->lo, hi = c->hi;
   const int parity = (int)(c->comm.epoch & 1);
-  const unsigned long long target = c->comm.epoch / 2 + 1;  // arrivals per rank for this parity
+  const unsigned long long target = c->comm.epoch / 2 + 1 + c->p2p_extra;  // arrivals per rank
   int rc;
   const bool hobi = c->scheme == kHobi;
   if (hi > lo) {
@@ -722,7 +738,7 @@ static int matvec_p2p(hobi_ctx* c, const double* u_dev, double* out_dev) {
       c->phys.diag1, c->phys.diag2, c->p2p_peers.p, c->comm.nranks, c->comm.rank, parity,
       c->p2p_done.p);
   p2p_wait_copy_kernel<<<std::max(1u, nblk(2 * c->nt, 1024)), 256, 0, c->stream>>>(
-      c->p2p_area.p, c->nt, c->comm.nranks, parity, target, out_dev);
+      c->p2p_area.p, c->nt, c->comm.nranks, parity, target, c->p2p_timeout_ns, c->p2p_err_dev, out_dev);
   c->launches += 2;
   HOBI_CUDA(cudaGetLastError());
   c->comm.epoch++;
@@ -749,6 +765,14 @@ int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
     if ((rc = comm_allgather(c))) return rc;
   }
   return gather_permute(c, out_dev);
+}
+
+// Called after a synchronisation: did a P2P wait give up on a peer?
+int p2p_check(hobi_ctx* c) {
+  if (c->comm.p2p && c->p2p_err && *reinterpret_cast<volatile int*>(c->p2p_err))
+    return fail(HOBI_ERR_NCCL,
+                "P2P gather: rows of a peer rank did not arrive within HOBI_P2P_TIMEOUT_MS");
+  return 0;
 }
 
 int gather_permute(hobi_ctx* c, double* out_dev) {

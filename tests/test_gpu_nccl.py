@@ -72,3 +72,29 @@ def test_single_rank_p2p_fused_gather(monkeypatch):
     with make_operator(plain, cfg) as op:
         sol0 = gmres_solve(op, assemble_rhs(plain), cfg)
     assert np.array_equal(sol.vector, sol0.vector)
+
+
+def test_p2p_missing_peer_times_out_instead_of_hanging(monkeypatch):
+    """A peer whose rows never arrive (test hook: wait for one arrival more than
+    any rank sends) must not wedge the GPU: the wait kernel's watchdog gives up
+    after HOBI_P2P_TIMEOUT_MS and the call reports a collective failure."""
+    import time
+
+    from paper_1301_5914_b200 import ChargeSystem, FlatMesh, PhysicalParams, SolverConfig, discretize, matvec_hobi
+    from paper_1301_5914_b200 import _native as N
+    from paper_1301_5914_b200.distributed import init_p2p_gather
+
+    g = golden("star_l2")
+    prob = discretize(FlatMesh(g["vertices"], g["normals"], g["faces"]), PhysicalParams(*g["params"]),
+                      ChargeSystem(g["qpos"], g["q"]), SolverConfig(workers=1))
+    lib = N.load()
+    uid = (C.c_ubyte * 128)()
+    N.check(lib.hobi_comm_init(prob.handle, uid, 1, 0))
+    monkeypatch.setenv("HOBI_P2P_TIMEOUT_MS", "300")
+    monkeypatch.setenv("HOBI_P2P_TEST_MISSING_ARRIVALS", "1")
+    init_p2p_gather(prob.handle, 0, 1)
+    t0 = time.monotonic()
+    with pytest.raises(RuntimeError, match="did not arrive"):
+        matvec_hobi(prob, g["u"])
+    assert time.monotonic() - t0 < 30.0
+    prob.close()
