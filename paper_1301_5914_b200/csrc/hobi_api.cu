@@ -756,9 +756,9 @@ int hobi_bench(hobi_ctx* c, const double* u, double* out, int steps, int mode, i
   DevBuf<unsigned char> scratch;
   const size_t flush_bytes = (size_t)512 << 20;
   if (flush_l2 && scratch.alloc(flush_bytes)) return HOBI_ERR_CUDA;
-  cudaEvent_t e0, e1;
-  HOBI_CUDA(cudaEventCreate(&e0));
-  HOBI_CUDA(cudaEventCreate(&e1));
+  EventPair ev;
+  HOBI_CUDA(ev.create());
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   int rc = 0;
   if (mode == 0) HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, bytes, cudaMemcpyHostToDevice, c->stream));
   for (int i = 0; i < steps && !rc; ++i) {
@@ -779,8 +779,6 @@ int hobi_bench(hobi_ctx* c, const double* u, double* out, int steps, int mode, i
     HOBI_CUDA(cudaMemcpyAsync(out, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
     HOBI_CUDA(cudaStreamSynchronize(c->stream));
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   return rc;
 }
 
@@ -806,9 +804,9 @@ int hobi_bench_rows(hobi_ctx* c, const double* u, int64_t lo, int64_t hi, int st
   DevBuf<unsigned char> scratch;
   const size_t flush_bytes = (size_t)512 << 20;
   if (flush_l2 && scratch.alloc(flush_bytes)) return HOBI_ERR_CUDA;
-  cudaEvent_t e0, e1;
-  HOBI_CUDA(cudaEventCreate(&e0));
-  HOBI_CUDA(cudaEventCreate(&e1));
+  EventPair ev;
+  HOBI_CUDA(ev.create());
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, 2 * c->nt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   int rc = 0;
   for (int i = 0; i < steps && !rc; ++i) {
@@ -822,8 +820,6 @@ int hobi_bench_rows(hobi_ctx* c, const double* u, int64_t lo, int64_t hi, int st
     HOBI_CUDA(cudaEventElapsedTime(&t, e0, e1));
     ms[i] = t;
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   return rc;
 }
 
@@ -869,9 +865,9 @@ extern "C" int hobi_probe_fp64_tflops(int device, double ms, double* tflops) {
   DevBuf<double> d;
   if (d.alloc(1)) return HOBI_ERR_CUDA;
   const int blocks = sms * 8, threads = 256, iters = 2048;
-  cudaEvent_t e0, e1;
-  HOBI_CUDA(cudaEventCreate(&e0));
-  HOBI_CUDA(cudaEventCreate(&e1));
+  EventPair ev;
+  HOBI_CUDA(ev.create());
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   for (int w = 0; w < 3; ++w) dfma_probe_kernel<<<blocks, threads>>>(d.p, iters, 0.999999, 1e-7);
   HOBI_CUDA(cudaDeviceSynchronize());
   double total_ms = 0.0, flops = 0.0;
@@ -887,8 +883,6 @@ extern "C" int hobi_probe_fp64_tflops(int device, double ms, double* tflops) {
     total_ms += t;
     flops = 2.0 * 32.0 * iters * (double)blocks * threads;
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   *tflops = flops / (best * 1e-3) * 1e-12;
   return 0;
 }

@@ -46,6 +46,19 @@ int cuda_fail(cudaError_t e, const char* what);
     if (e_ != cudaSuccess) return hobi::cuda_fail(e_, #call); \
   } while (0)
 
+// A pair of timing events destroyed on every exit path.
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaError_t create() {
+    cudaError_t e = cudaEventCreate(&a);
+    return e != cudaSuccess ? e : cudaEventCreate(&b);
+  }
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
