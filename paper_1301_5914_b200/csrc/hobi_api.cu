@@ -135,6 +135,11 @@ static int common_init(hobi_ctx* c, int device, double eps1, double eps2, double
   HOBI_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   HOBI_CUDA(cudaEventCreate(&c->ev0));
   HOBI_CUDA(cudaEventCreate(&c->ev1));
+  if (const char* v = getenv("HOBI_SWEEP_VARIANT")) {  // tuning: default tile, still auto-switched
+    const int vi = atoi(v);
+    if (vi < 0 || vi >= sweep_variant_count()) return fail(HOBI_ERR_VALUE, "HOBI_SWEEP_VARIANT out of range");
+    c->sweep_variant = vi;
+  }
   Physics& p = c->phys;
   p.eps1 = eps1;
   p.eps2 = eps2;
