@@ -55,7 +55,7 @@ def unpack_gathered(recv: np.ndarray, n: int, nranks: int) -> np.ndarray:
     return np.concatenate([recv[r, 0, v - lo], recv[r, 1, v - lo]])
 
 
-def init_nccl_comm(handle, rank: int, world: int) -> None:
+def init_nccl_comm(handle, rank: int, world: int, device: int | None = None) -> None:
     """Create the library's NCCL communicator: rank 0 draws the unique id,
     torch.distributed broadcasts the 128 bytes, every rank joins.  With
     HOBI_GATHER=p2p the gather is then switched to the fused epilogue +
@@ -63,6 +63,14 @@ def init_nccl_comm(handle, rank: int, world: int) -> None:
     import torch.distributed as dist
 
     from . import _native as N
+
+    if device is not None and dist.get_backend() == "nccl":
+        # torch's NCCL collectives run on torch's current device: make it this
+        # rank's GPU, or every rank would broadcast from device 0
+        import torch
+
+        if torch.cuda.current_device() != device:
+            torch.cuda.set_device(device)
 
     lib = N.load()
     uid = (C.c_ubyte * 128)()

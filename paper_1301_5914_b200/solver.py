@@ -282,7 +282,7 @@ def discretize(mesh: FlatMesh, params: PhysicalParams, charges: ChargeSystem,
         from .distributed import init_nccl_comm
 
         try:
-            init_nccl_comm(handle.ptr, rank, world)
+            init_nccl_comm(handle.ptr, rank, world, _device_index())
         except N.NativeError as exc:
             _raise(exc.status)
     return DiscretizedProblem(mesh, params, charges, config.scheme, handle, rule, duffy, (rank, world))
@@ -323,7 +323,7 @@ def problem_from_caches(reference_problem, config: SolverConfig | None = None) -
     if world > 1:
         from .distributed import init_nccl_comm
 
-        init_nccl_comm(handle.ptr, rank, world)
+        init_nccl_comm(handle.ptr, rank, world, _device_index())
     mesh = FlatMesh(m.vertices, m.normals, m.faces)
     charges = ChargeSystem(rp.charges.positions, rp.charges.charges)
     prob = DiscretizedProblem(mesh, p, charges, "hobi", handle, _rule_of(arr["reg_bary"]),
