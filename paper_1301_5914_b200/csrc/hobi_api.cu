@@ -111,7 +111,9 @@ static int setup_gather(hobi_ctx* c, int nranks) {
 
 // ---------------------------------------------------------------------------
 // source-group partition: a function of the problem size only (never of the
-// row split), chosen so an 8-way split still fills 148 SMs several times.
+// row split or the tuned tile), chosen so an 8-way split still fills 148 SMs
+// several times.  768 rows is a fixed reference tile for that sizing, not the
+// sweep's tile: retuning the sweep must not move group boundaries.
 
 static int choose_groups(hobi_ctx* c) {
   c->n_src_tiles = (int)(c->ns_pad / kSrcTile);

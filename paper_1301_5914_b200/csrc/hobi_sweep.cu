@@ -633,8 +633,8 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
 // of B tiles come first; the end of the source axis is cut into groups that
 // halve in size (B/2, B/2, B/4, B/4, ..., 1, 1), so the group-major work queue
 // of the persistent sweep ends with small items and the dynamic tail is short.
-// B gives an 8-way split with `tiles8` target tiles per rank ~16 work items
-// per resident CTA slot (2 per SM x 148 SMs).
+// B gives an 8-way split with `tiles8` reference tiles per rank ~16 work
+// items per 2 x 148 CTA slots (more with the tuned 3-CTA/SM, 512-row tile).
 std::vector<int2> make_groups(int n_src_tiles, int64_t tiles8) {
   std::vector<int2> g;
   if (n_src_tiles <= 0) return g;
