@@ -375,14 +375,15 @@ __global__ void __launch_bounds__(kEpiRows* kEpiSlices) epilogue_p2p_kernel(
   }
 }
 
-// Wait until all ranks' rows of this epoch have arrived, then hand the
-// gathered vector to the caller's buffer.
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 
+// Wait until all ranks' rows of this epoch have arrived, then hand the
+// gathered vector to the caller's buffer.  A watchdog bounds the wait: after
+// timeout_ns the kernel raises *err (mapped host memory) and exits.
 __global__ void p2p_wait_copy_kernel(const double* __restrict__ area, int64_t nt, int nranks, int parity,
                                      unsigned long long target, unsigned long long timeout_ns,
                                      int* err, double* __restrict__ out) {
