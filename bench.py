@@ -43,6 +43,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BIE matvec pair-interactions/s (FP64) and GMRES solve time at 1/2/4/8 B200"
 FLOPS_PER_PAIR = 96  # SURVEY.md 8(d) canonical accounting
+# FP64 instructions the default sweep executes per pair (26 DFMA + 13 DMUL + 5 DADD;
+# SASS count, checked against the built library by tests/test_cabi.py)
+FP64_INSTR_PER_PAIR = 44
 
 
 def _args():
@@ -344,6 +347,15 @@ def run_ours(a):
                 traffic = t["bytes_per_launch"]
         except Exception:  # noqa: BLE001
             traffic = None
+    # executed-instruction view of the same launches: FP64 lane-ops per clock
+    # per SM against the pipe's 64 (the canonical-flop frac above is the headline)
+    clk = clocks.summary()
+    pipe = None
+    sms = C.c_int(0)
+    if clk.get("sm_mhz") and lib.hobi_device_sms(int(os.environ["HOBI_DEVICE"]), C.byref(sms)) == 0:
+        ops = FP64_INSTR_PER_PAIR * local_pairs / (sweep_avg * 1e-3) / (sms.value * clk["sm_mhz"] * 1e6)
+        pipe = {"instr_per_pair": FP64_INSTR_PER_PAIR, "lane_ops_per_clk_per_sm": ops,
+                "frac_of_64": ops / 64.0, "sms": sms.value, "sm_mhz": clk["sm_mhz"]}
     if rank == 0:
         conf = _workload(cfg, nv, nf, nq)
         conf["parallelism"] = (f"row split x{world} + " + ("NCCL allgather" if a.gather == "nccl" else
@@ -362,9 +374,10 @@ def run_ours(a):
                          "kernel": "sweep_kernel<kScreened,FULL>", "flops_per_pair": FLOPS_PER_PAIR,
                          "avg_launch_ms": sweep_avg, "pairs_per_launch": local_pairs,
                          "peak_source": "DFMA probe in this run (hobi_probe_fp64_tflops); "
-                                        "MEASURED_PEAKS.json has no FP64 entry"},
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "fp64_pipe": pipe},
             "gpu_launches": int(launches.value),
-            "clocks": clocks.summary(),
+            "clocks": clk,
             "solve": solve,
             "split_model": split_model,
             "cpu_baseline": cpu,

@@ -41,6 +41,8 @@ typedef struct hobi_ctx hobi_ctx;
 const char* hobi_last_error(void);
 int hobi_abi_version(void);
 int hobi_device_count(int* count);
+/* Streaming multiprocessors of a device (roofline bookkeeping). */
+int hobi_device_sms(int device, int* sms);
 
 /*
  * Build every discretisation cache on `device`: curved cubic nodes for the

@@ -30,6 +30,7 @@ SIGNATURES = {
     "hobi_last_error": (C.c_char_p, []),
     "hobi_abi_version": (C.c_int, []),
     "hobi_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "hobi_device_sms": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
     "hobi_create": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _i64p, C.c_int64, C.c_double, C.c_double,
                               C.c_double, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp, C.c_int,
                               C.POINTER(_ctxp)]),

@@ -222,6 +222,12 @@ int hobi_device_count(int* count) {
   return 0;
 }
 
+int hobi_device_sms(int device, int* sms) {
+  *sms = 0;
+  HOBI_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, device));
+  return 0;
+}
+
 int hobi_create(int device, const double* vertices, const double* normals, int64_t nv,
                 const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
                 const double* reg_pts, const double* reg_wts, const double* reg_shape, int nq,

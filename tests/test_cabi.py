@@ -44,6 +44,32 @@ def test_library_is_sm100a_only():
     assert "sm_100a" in out.stdout
 
 
+def test_default_sweep_executes_the_documented_instruction_mix():
+    """bench.py's FP64_INSTR_PER_PAIR and DESIGN.md's 26 DFMA + 13 DMUL + 5 DADD
+    are the SASS of the default sweep variant (step_R4_minb3_unroll2: 4
+    targets x 2 unrolled sources = 8 pairs per loop body, nothing else FP64)."""
+    import subprocess
+
+    import bench
+
+    internal = open(os.path.join(ROOT, "paper_1301_5914_b200", "csrc", "hobi_internal.cuh")).read()
+    assert re.search(r"int sweep_variant = 15;.*step_R4_minb3_unroll2", internal)
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", N.LIB_PATH], capture_output=True,
+                         text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    body, on = [], False
+    for line in out.stdout.splitlines():
+        if "Function : " in line:
+            on = "sweep_kernelILi1ELb1ELb0ELi4ELi3ELi2ELb1E" in line
+        elif on:
+            body.append(line)
+    sass = "\n".join(body)
+    counts = {op: len(re.findall(r"\b" + op + r"\b", sass)) for op in ("DFMA", "DMUL", "DADD")}
+    assert counts == {"DFMA": 26 * 8, "DMUL": 13 * 8, "DADD": 5 * 8}, counts
+    assert bench.FP64_INSTR_PER_PAIR == 44
+
+
 def test_no_cpu_fallback_without_device():
     if N.device_count() > 0:
         pytest.skip("a GPU is present")
