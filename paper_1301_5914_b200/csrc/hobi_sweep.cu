@@ -497,12 +497,16 @@ static const SweepVariant kVariants[] = {
     HOBI_V(2, 1, 2), HOBI_V(2, 6, 2), HOBI_V(4, 3, 2), HOBI_V(1, 8, 2), HOBI_V(4, 3, 1),
     HOBI_V(4, 4, 1), HOBI_V(3, 4, 1), HOBI_V(6, 2, 1), HOBI_V(8, 2, 1), HOBI_V(3, 4, 2),
     HOBI_V(4, 4, 2), HOBI_V(5, 3, 1), HOBI_VS(6, 2, 1), HOBI_VS(4, 3, 1), HOBI_VS(3, 4, 1),
-    HOBI_VS(4, 3, 2),
+    HOBI_VS(4, 3, 2), HOBI_VS(4, 3, 4), HOBI_VS(6, 2, 2), HOBI_VS(3, 4, 2), HOBI_VS(5, 3, 2),
+    HOBI_VS(8, 2, 2),
 };
 #undef HOBI_V
 #undef HOBI_VS
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
-constexpr int kSmallVariant = 3;  // R1_minb8_unroll2
+constexpr int kSmallVariant = 3;   // R1_minb8_unroll2
+constexpr int kWideVariant = 17;   // step_R6_minb2_unroll2: 768-row tiles, the default
+constexpr int kNarrowVariant = 15; // step_R4_minb3_unroll2: 512-row tiles
+static_assert(kWideVariant < kNumVariants && kNarrowVariant < kNumVariants, "variant table");
 
 // Physics folded into the per-source record and the launch constants Ap, Bp
 // (see hobi_fastmath.cuh).
@@ -553,6 +557,15 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
       seg[0].fn = sweep_kernel<kScreened, true, true, kSweepR, 1, 2>;
     else if (full) {
       int vi = c->sweep_variant;
+      // the wide tile is ~1% faster per pair, but a range that leaves more
+      // than 2% of its rows past the last whole 768-row tile (an 8-way split
+      // of config 4 leaves 513 of 5121) runs better on 512-row tiles
+      if (!c->variant_pinned && vi == kWideVariant) {
+        const int64_t rows = t1 - t0;
+        const int64_t rem_w = rows % (kSweepThreads * kVariants[kWideVariant].r);
+        const int64_t rem_n = rows % (kSweepThreads * kVariants[kNarrowVariant].r);
+        if (rem_w * 50 > rows && rem_n < rem_w) vi = kNarrowVariant;
+      }
       // small problems: if the tuned tile leaves too few work items for 148
       // SMs, use 128-row tiles (same sums bitwise, more parallelism)
       const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * kVariants[vi].r) * n_groups;

@@ -46,27 +46,31 @@ def test_library_is_sm100a_only():
 
 def test_default_sweep_executes_the_documented_instruction_mix():
     """bench.py's FP64_INSTR_PER_PAIR and DESIGN.md's 26 DFMA + 13 DMUL + 5 DADD
-    are the SASS of the default sweep variant (step_R4_minb3_unroll2: 4
-    targets x 2 unrolled sources = 8 pairs per loop body, nothing else FP64)."""
+    are the SASS of the default sweep variants: step_R6_minb2_unroll2 (6
+    targets x 2 unrolled sources = 12 pairs per loop body, nothing else FP64)
+    and step_R4_minb3_unroll2 (8 pairs), used when a row range leaves a long
+    remainder past the 768-row tiles."""
     import subprocess
 
     import bench
 
     internal = open(os.path.join(ROOT, "paper_1301_5914_b200", "csrc", "hobi_internal.cuh")).read()
-    assert re.search(r"int sweep_variant = 15;.*step_R4_minb3_unroll2", internal)
+    assert re.search(r"int sweep_variant = 17;.*step_R6_minb2_unroll2", internal)
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", N.LIB_PATH], capture_output=True,
                          text=True)
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
-    body, on = [], False
-    for line in out.stdout.splitlines():
-        if "Function : " in line:
-            on = "sweep_kernelILi1ELb1ELb0ELi4ELi3ELi2ELb1E" in line
-        elif on:
-            body.append(line)
-    sass = "\n".join(body)
-    counts = {op: len(re.findall(r"\b" + op + r"\b", sass)) for op in ("DFMA", "DMUL", "DADD")}
-    assert counts == {"DFMA": 26 * 8, "DMUL": 13 * 8, "DADD": 5 * 8}, counts
+    for frag, pairs in (("sweep_kernelILi1ELb1ELb0ELi6ELi2ELi2ELb1E", 12),
+                        ("sweep_kernelILi1ELb1ELb0ELi4ELi3ELi2ELb1E", 8)):
+        body, on = [], False
+        for line in out.stdout.splitlines():
+            if "Function : " in line:
+                on = frag in line
+            elif on:
+                body.append(line)
+        sass = "\n".join(body)
+        counts = {op: len(re.findall(r"\b" + op + r"\b", sass)) for op in ("DFMA", "DMUL", "DADD")}
+        assert counts == {"DFMA": 26 * pairs, "DMUL": 13 * pairs, "DADD": 5 * pairs}, (frag, counts)
     assert bench.FP64_INSTR_PER_PAIR == 44
 
 
