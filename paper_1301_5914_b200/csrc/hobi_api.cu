@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -176,6 +177,19 @@ static int alloc_operands(hobi_ctx* c) {
   return 0;
 }
 
+// HOBI_TRACE_INIT=1: wall time of each stage of context creation (stderr).
+struct InitTrace {
+  bool on = getenv("HOBI_TRACE_INIT") && getenv("HOBI_TRACE_INIT")[0] == '1';
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t s = nullptr) {
+    if (!on) return;
+    if (s) cudaStreamSynchronize(s);
+    auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "hobi init %-16s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 // Scale check for the table-driven exp (valid for kappa*r < 1e12).
 static int check_extent(hobi_ctx* c, const double* v, int64_t n) {
   if (c->phys.mode != kScreened) return 0;
@@ -243,6 +257,7 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
     if (faces[i] < 0 || faces[i] >= nv)
       return fail(HOBI_ERR_VALUE, "face " + std::to_string(i / 3) + " references a vertex outside [0, " +
                                       std::to_string(nv) + ")");
+  InitTrace tr;
   hobi_ctx* c = new hobi_ctx();
   int rc;
   auto bail = [&](int r) {
@@ -250,6 +265,7 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
     return r;
   };
   if ((rc = common_init(c, device, eps1, eps2, kappa))) return bail(rc);
+  tr.mark("common_init", c->stream);
   if ((rc = check_extent(c, vertices, nv))) return bail(rc);
   c->scheme = kHobi;
   c->nv = nv;
@@ -309,9 +325,12 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
   if (!e) e = up(c->reg_bary.p, rbary.data(), 3 * nq * sizeof(double));
   if (!e) e = up(c->duf_bary.p, dbary.data(), 3 * nd * sizeof(double));
   if (e) return bail(cuda_fail(e, "cudaMemcpyAsync(upload)"));
+  tr.mark("alloc+upload", c->stream);
   if ((rc = upload_rule_tables(reg_shape, nq, duf_shape, nd, reg_wts, duf_wts))) return bail(rc);
+  tr.mark("rule tables", c->stream);
   int bad_slot = -1, bad_code = 0;
   if ((rc = build_geometry(c, slot_to_pair.data(), &bad_slot, &bad_code))) return bail(rc);
+  tr.mark("geometry", c->stream);
   if (bad_slot >= 0) {
     static const char* msgs[] = {"", "arc endpoints coincide",
                                  "endpoint normal is nearly parallel to the chord",
@@ -320,6 +339,7 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
                      "face " + std::to_string(bad_slot / 3) + ": " + msgs[bad_code & 3]));
   }
   if ((rc = alloc_operands(c))) return bail(rc);
+  tr.mark("operands", c->stream);
   *out = c;
   return 0;
 }

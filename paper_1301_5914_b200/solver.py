@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -97,7 +98,12 @@ class SurfaceSolution:
 
 
 def _world():
-    """(rank, world_size, local_rank) of an initialised torch.distributed job."""
+    """(rank, world_size, local_rank) of an initialised torch.distributed job.
+
+    A job that never imported torch cannot have initialised torch.distributed,
+    so torch (seconds to import) is only consulted when already loaded."""
+    if "torch" not in sys.modules:
+        return 0, 1, 0
     try:
         import torch.distributed as dist
     except Exception:  # noqa: BLE001
@@ -108,6 +114,8 @@ def _world():
 
 
 def _dist_initialized() -> bool:
+    if "torch" not in sys.modules:
+        return False
     try:
         import torch.distributed as dist
     except Exception:  # noqa: BLE001
