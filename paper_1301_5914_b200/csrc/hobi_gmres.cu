@@ -7,6 +7,7 @@
 // triangular solve stay on the host in the reference's exact scalar order.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -153,7 +154,7 @@ int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
     ws.n = -1;
     if (ws.V.alloc((size_t)(m + 1) * ws.ldv) || ws.w.alloc(n) || ws.x.alloc(n) || ws.r.alloc(n) ||
         ws.b.alloc(n) || ws.part.alloc(2 * ws.grid) || ws.hcol.alloc(m + 2) || ws.nrm.alloc(1) ||
-        ws.y.alloc(m))
+        ws.y.alloc(m) || ws.hcol_h.alloc(m + 2) || ws.nrm_h.alloc(1))
       return HOBI_ERR_CUDA;
     ws.n = n;
     ws.m = m;
@@ -165,8 +166,9 @@ int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
     norm_finish_kernel<<<1, 32, 0, stream>>>(ws.part.p, ws.grid, ws.nrm.p);
     launches += 2;
     HOBI_CUDA(cudaGetLastError());
-    HOBI_CUDA(cudaMemcpyAsync(val, ws.nrm.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    HOBI_CUDA(cudaMemcpyAsync(ws.nrm_h.p, ws.nrm.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
     HOBI_CUDA(cudaStreamSynchronize(stream));
+    *val = ws.nrm_h.p[0];
     return 0;
   };
   int rc;
@@ -236,9 +238,10 @@ int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,
                                               stream));
         launches++;
       }
-      HOBI_CUDA(cudaMemcpyAsync(hcol.data(), ws.hcol.p, (j + 2) * sizeof(double),
+      HOBI_CUDA(cudaMemcpyAsync(ws.hcol_h.p, ws.hcol.p, (j + 2) * sizeof(double),
                                 cudaMemcpyDeviceToHost, stream));
       HOBI_CUDA(cudaStreamSynchronize(stream));
+      std::copy(ws.hcol_h.p, ws.hcol_h.p + j + 2, hcol.begin());
       if (trace) {
         double tc = now();
         t_mv += tb - ta;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -79,6 +80,27 @@ struct DevBuf {
   ~DevBuf() { release(); }
 };
 
+// Page-locked host buffer (small per-iteration device->host reads).
+template <typename T>
+struct HostBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int alloc(size_t count) {
+    release();
+    n = count;
+    if (count == 0) return 0;
+    cudaError_t e = cudaMallocHost(&p, count * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+    return 0;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~HostBuf() { release(); }
+};
+
 // Constant physics, folded per scheme.
 struct Physics {
   double eps1, eps2, kappa, er, ier;
@@ -102,6 +124,7 @@ struct Comm {
 // every solve showed 0.1-0.3 s stalls on the B200 hosts.
 struct GmresWorkspace {
   DevBuf<double> V, w, x, r, b, part, hcol, nrm, y;
+  HostBuf<double> hcol_h, nrm_h;  // pinned landing slots of the per-step reads
   int64_t n = -1, ldv = 0;
   int m = -1, grid = 1;
 };
@@ -167,6 +190,9 @@ struct hobi_ctx {
   // instrumentation
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> ev_pool;   // recorded sweep brackets, read lazily
+  // launch bookkeeping cached per sweep instantiation: (kernel, CTAs per SM)
+  std::vector<std::pair<const void*, int>> occupancy;
+  int sms = 0;
   size_t ev_used = 0;                  // pairs of ev_pool in flight
   double sweep_ms = 0.0;
   int64_t sweep_launches = 0;

@@ -586,8 +586,8 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
                      : (full ? sweep_kernel<kLaplace, true, false, kSweepR, 1, 2>
                              : sweep_kernel<kLaplace, false, false, kSweepR, 1, 2>);
   }
-  int sms = 0;
-  HOBI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+  if (!c->sms) HOBI_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
+  const int sms = c->sms;
   const WeightConstants wc = weight_constants(c->phys);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {  // brackets are read lazily by collect_sweep_timing: no sync here
@@ -616,9 +616,14 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
     const Seg& sg = seg[k];
     cudaStream_t st = k == 1 ? c->side : c->stream;
     unsigned* ticket = k == 1 ? c->ticket.p + 1 : c->ticket.p;
-    HOBI_CUDA(cudaFuncSetAttribute(sg.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
-    int per_sm = 0;
-    HOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sg.fn, kSweepThreads, kSweepSmem));
+    int per_sm = -1;
+    for (const auto& o : c->occupancy)
+      if (o.first == (const void*)sg.fn) per_sm = o.second;
+    if (per_sm < 0) {
+      HOBI_CUDA(cudaFuncSetAttribute(sg.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem));
+      HOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sg.fn, kSweepThreads, kSweepSmem));
+      c->occupancy.emplace_back((const void*)sg.fn, per_sm);
+    }
     const int64_t items = (int64_t)nblk(sg.b - sg.a, kSweepThreads * sg.r) * n_groups;
     const unsigned grid =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)std::max(per_sm, 1) * sms));
