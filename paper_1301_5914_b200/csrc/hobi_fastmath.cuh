@@ -2,9 +2,9 @@
 // for the B200 FP64 pipe.  See DESIGN.md "kernel algebra" for the derivation:
 // coordinates are pre-scaled by kappa so r' = kappa*r, the physical constants
 // (1/4pi, kappa^n, er, 1/er) are folded into the per-source record (the wp
-// weight rides on the source normal) and two launch constants, e^{-kr} comes
-// from one table-driven range reduction, and 1/r from the MUFU rsqrt seed
-// plus one third-order Newton step.  44 FP64 instructions per pair
+// weight rides on the source normal) and two launch constants, expm1 and exp
+// share one table-driven range reduction, and 1/r comes from the MUFU rsqrt
+// seed plus one third-order Newton step.  45 FP64 instructions per pair
 // (vs ~95 for a literal libdevice transcription of kernels.py:112-130).
 #pragma once
 
@@ -26,16 +26,18 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   return fma(ye, c, y);
 }
 
-// exp(-x) for 0 <= x < 1e12 as S (1 + p), with S = 2^(k/2048) from a
-// 2048-entry table (shared memory, exponent patched in integer registers) and
-// p = e^f - 1 on |f| <= ln2/4096 (degree-3 Taylor, truncation < 4e-17).
-// 7 FP64 ops.  The pair algebra needs e^{-kr} itself: em1 = E - 1 only ever
-// appears multiplied into terms whose absolute rounding error it does not
-// raise above the row sum's.
-__device__ __forceinline__ double exp_neg(double x, const double* __restrict__ etab) {
-  const double kInv = 2954.6394437405970;
-  const double kMagic = 6755399441055744.0;
-  const double kStep = 3.3845077175778578e-4;
+// exp(-x) - 1 for 0 <= x < 1e12, computed as S(1+p) - 1 with S = 2^(k/2048)
+// from a 2048-entry table (shared memory) and p = e^f - 1 on |f| <= ln2/4096
+// (degree-3 Taylor, truncation < 4e-17).  S - 1 is exact for S in [1/2, 1]
+// (Sterbenz), so small arguments keep expm1's relative accuracy.  8 FP64 ops.
+// K1 = W1 (e^{-kr} - 1)/r needs that accuracy: with kr << 1 and a zero phi
+// block, or eps2 ~ eps1, whole rows and the energy are K1 sums (an
+// exp-only variant, E - 1 formed after rounding E, lost up to 1e-6 there;
+// tests/test_gpu_parity.py::test_small_screening_keeps_expm1_accuracy).
+__device__ __forceinline__ double expm1_neg(double x, const double* __restrict__ etab) {
+  const double kInv = 2954.6394437405970;      // 2048/ln2
+  const double kMagic = 6755399441055744.0;    // 1.5*2^52: rounds to integer in the low word
+  const double kStep = 3.3845077175778578e-4;  // ln2/2048
   double kf = fma(-x, kInv, kMagic);
   int k = __double2loint(kf);
   double kd = kf - kMagic;
@@ -47,7 +49,7 @@ __device__ __forceinline__ double exp_neg(double x, const double* __restrict__ e
   int n = k >> kExpShift;
   double S = __hiloint2double(__double2hiint(T) + (n << 20), __double2loint(T));
   S = (n < -1000) ? 0.0 : S;
-  return fma(S, p, S);
+  return fma(S, p, S - 1.0);
 }
 
 // Screened pair (kappa > 0), scaled coordinates.  Source record:
@@ -55,12 +57,11 @@ __device__ __forceinline__ double exp_neg(double x, const double* __restrict__ e
 //   W1 = -k wd/4pi, C = k^2 wd/(4pi er), D = -k^2 (1-1/er) wd/4pi,
 // and two launch constants Ap = er/k, Bp = (er-1)/k (so M (a Ap + Bp) =
 // k^2 wp (a er + er - 1)/4pi).  With dny' = d.m' = M dny, u = dny'/r^2:
-//   K1 wd + K2 wp = (1/r) (W1 (E - 1) + u (a Ap + Bp))
+//   K1 wd + K2 wp = (1/r) (W1 em1 + u (a Ap + Bp))
 //   K3 wd + K4 wp = (1/r^3) (dnx (t2 - u b) + a nn')
-// where E = e^{-kr}, a = (1+kr)E - 1, b = 3a + (kr)^2 E (kernels.py:119-120),
-// t2 = a C + D, nn' = n.m'.
+// where t2 = a C + D, b = 3a + kr*kre (kernels.py:119-120), nn' = n.m'.
 // acc1 += K1 wd + K2 wp ; acc2 += K3 wd + K4 wp   (solver.py:333-334)
-// 44 FP64 instructions per pair (26 DFMA, 13 DMUL, 5 DADD).
+// 45 FP64 instructions per pair (25 DFMA, 14 DMUL, 6 DADD).
 template <bool FULL>
 __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, double nx, double ny,
                                               double nz, double sx, double sy, double sz, double mx,
@@ -73,15 +74,16 @@ __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, d
   double ir = rsqrt_fast(r2);
   double r = r2 * ir;  // kappa * |x - y|
   double ir2 = ir * ir;
-  double E = exp_neg(r, etab);    // e^{-kr}
-  double a = fma(r, E, E) - 1.0;  // (1+kr)e^{-kr} - 1      (kernels.py:119)
+  double em1 = expm1_neg(r, etab);
+  double kre = fma(r, em1, r);  // kr e^{-kr}
+  double a = em1 + kre;         // (1+kr)e^{-kr} - 1      (kernels.py:119)
   double u = dny * ir2;
   double t = fma(a, Ap, Bp);
-  acc1 = fma(ir, fma(E, W1, fma(u, t, -W1)), acc1);  // W1 (E - 1) + u t
+  acc1 = fma(ir, fma(em1, W1, u * t), acc1);
   if (FULL) {
     double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
     double nn = fma(nx, mx, fma(ny, my, nz * mz));
-    double b = fma(a, 3.0, r2 * E);  // 3a + kr*kr e^{-kr}   (kernels.py:120)
+    double b = fma(a, 3.0, r * kre);  // kernels.py:120
     double g = fma(-u, b, fma(a, C, D));
     double X = fma(dnx, g, a * nn);
     acc2 = fma(ir, X * ir2, acc2);
@@ -99,7 +101,7 @@ __device__ __forceinline__ void pairs_screened_stepmajor(
     const double (&ny)[R], const double (&nz)[R], double sx, double sy, double sz, double mx, double my,
     double mz, double W1, double C, double D, double Ap, double Bp, const double* __restrict__ etab,
     double (&acc1)[R], double (&acc2)[R]) {
-  double dx[R], dy[R], dz[R], r2[R], dny[R], dnx[R], nn[R], ir[R], r[R], E[R], a[R];
+  double dx[R], dy[R], dz[R], r2[R], dny[R], dnx[R], nn[R], ir[R], r[R], em1[R], a[R], kre[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) dx[q] = tx[q] - sx;
 #pragma unroll
@@ -128,9 +130,12 @@ __device__ __forceinline__ void pairs_screened_stepmajor(
     r[q] = r2[q] * ir[q];
   }
 #pragma unroll
-  for (int q = 0; q < R; ++q) E[q] = exp_neg(r[q], etab);
+  for (int q = 0; q < R; ++q) em1[q] = expm1_neg(r[q], etab);
 #pragma unroll
-  for (int q = 0; q < R; ++q) a[q] = fma(r[q], E[q], E[q]) - 1.0;
+  for (int q = 0; q < R; ++q) {
+    kre[q] = fma(r[q], em1[q], r[q]);
+    a[q] = em1[q] + kre[q];
+  }
   double ir2[R], u[R], t[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) {
@@ -140,16 +145,16 @@ __device__ __forceinline__ void pairs_screened_stepmajor(
 #pragma unroll
   for (int q = 0; q < R; ++q) t[q] = fma(a[q], Ap, Bp);
 #pragma unroll
-  for (int q = 0; q < R; ++q) t[q] = fma(u[q], t[q], -W1);
+  for (int q = 0; q < R; ++q) t[q] = u[q] * t[q];
 #pragma unroll
-  for (int q = 0; q < R; ++q) t[q] = fma(E[q], W1, t[q]);
+  for (int q = 0; q < R; ++q) t[q] = fma(em1[q], W1, t[q]);
 #pragma unroll
   for (int q = 0; q < R; ++q) acc1[q] = fma(ir[q], t[q], acc1[q]);
 #pragma unroll
   for (int q = 0; q < R; ++q) t[q] = fma(a[q], C, D);
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    const double b = fma(a[q], 3.0, r2[q] * E[q]);
+    const double b = fma(a[q], 3.0, r[q] * kre[q]);
     t[q] = fma(-u[q], b, t[q]);
   }
 #pragma unroll

@@ -466,3 +466,27 @@ def test_random_surfaces_against_oracle(seed):
     ol = O.discretize(mesh.vertices, mesh.normals, mesh.faces, e1, e2, kap, scheme="lobi")
     ul = rng.standard_normal(pl.n_unknowns)
     assert rel_l2(matvec_lobi(pl, ul), O.matvec(ol, ul)) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("kappa", [1e-12, 1e-9, 1e-6])
+def test_small_screening_keeps_expm1_accuracy(kappa):
+    """kappa*R << 1 with a zero phi block: the first output block is a pure
+    K1 sum, K1 = W1 (e^{-kr} - 1)/r, so e^{-kr} - 1 must keep expm1's relative
+    accuracy (an exp-only formulation lost up to 1e-6 here).  The same with
+    eps2 ~ eps1, where K2 no longer dominates mixed vectors."""
+    import hobi_oracle as O
+
+    g = golden("star_l2")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    rng = np.random.default_rng(17)
+    for e2 in (40.0, 1.0 + 1e-6):
+        prob = discretize(mesh, PhysicalParams(1.0, e2, kappa), ChargeSystem(np.zeros((0, 3)), []),
+                          SolverConfig())
+        o = O.discretize(g["vertices"], g["normals"], g["faces"], 1.0, e2, kappa)
+        T = prob.n_collocation
+        u = rng.standard_normal(2 * T)
+        u[:T] = 0.0
+        got, ref = matvec_hobi(prob, u), O.matvec(o, u)
+        assert rel_l2(got[:T], ref[:T]) <= 1e-13, (e2, rel_l2(got[:T], ref[:T]))
+        assert rel_l2(got[T:], ref[T:]) <= 1e-13
+        prob.close()
