@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -326,10 +327,17 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
   if (!e) e = up(c->duf_bary.p, dbary.data(), 3 * nd * sizeof(double));
   if (e) return bail(cuda_fail(e, "cudaMemcpyAsync(upload)"));
   tr.mark("alloc+upload", c->stream);
-  if ((rc = upload_rule_tables(reg_shape, nq, duf_shape, nd, reg_wts, duf_wts))) return bail(rc);
-  tr.mark("rule tables", c->stream);
   int bad_slot = -1, bad_code = 0;
-  if ((rc = build_geometry(c, slot_to_pair.data(), &bad_slot, &bad_code))) return bail(rc);
+  {
+    // the rule tables live in __constant__ memory shared by every context on
+    // the device: concurrent creations take turns until their geometry
+    // kernels have finished reading them (build_geometry synchronises)
+    static std::mutex rule_tables_mutex;
+    std::lock_guard<std::mutex> lock(rule_tables_mutex);
+    if ((rc = upload_rule_tables(reg_shape, nq, duf_shape, nd, reg_wts, duf_wts))) return bail(rc);
+    tr.mark("rule tables", c->stream);
+    if ((rc = build_geometry(c, slot_to_pair.data(), &bad_slot, &bad_code))) return bail(rc);
+  }
   tr.mark("geometry", c->stream);
   if (bad_slot >= 0) {
     static const char* msgs[] = {"", "arc endpoints coincide",

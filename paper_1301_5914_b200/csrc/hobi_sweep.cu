@@ -19,6 +19,8 @@
 // any number of GPUs (solver.py:12-17).
 #include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <vector>
 
 #include "hobi_fastmath.cuh"
 #include "hobi_internal.cuh"
@@ -27,10 +29,20 @@ namespace hobi {
 
 __device__ double g_exp_table[kExpTable];
 
+// Once per device (the table never changes; a sweep running in another
+// context reads it, so it is not rewritten under it).
 int upload_exp_table() {
+  static std::mutex m;
+  static std::vector<int> done;
+  int dev = 0;
+  HOBI_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(m);
+  if (dev < (int)done.size() && done[dev]) return 0;
   double t[kExpTable];
   for (int j = 0; j < kExpTable; ++j) t[j] = (double)exp2l((long double)j / kExpTable);
   HOBI_CUDA(cudaMemcpyToSymbol(g_exp_table, t, sizeof(t)));
+  if (dev >= (int)done.size()) done.resize(dev + 1, 0);
+  done[dev] = 1;
   return 0;
 }
 

@@ -490,3 +490,35 @@ def test_small_screening_keeps_expm1_accuracy(kappa):
         assert rel_l2(got[:T], ref[:T]) <= 1e-13, (e2, rel_l2(got[:T], ref[:T]))
         assert rel_l2(got[T:], ref[T:]) <= 1e-13
         prob.close()
+
+
+def test_concurrent_creation_with_different_rules():
+    """Contexts built concurrently from threads with different quadrature rules
+    (rule tables live in device constant memory) still get bitwise the
+    reference's caches."""
+    import threading
+
+    from paper_1301_5914_b200 import TriangleRule
+
+    g9, g4 = golden("star_l2_rule9"), golden("star_l2")
+    rule9 = TriangleRule(g9["rule_points"], g9["rule_weights"], "custom", int(g9["rule_degree"]))
+    errors = []
+
+    def build(g, kw):
+        try:
+            for _ in range(4):
+                prob = _problem(g, **kw)
+                for key in ("reg_pos", "reg_w", "duf_pos", "duf_w"):
+                    if not np.array_equal(getattr(prob, key), g[key]):
+                        errors.append(key)
+                prob.close()
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    kw9 = {"regular_rule": rule9, "duffy_points": int(g9["duffy"])}
+    threads = [threading.Thread(target=build, args=(g, kw)) for g, kw in ((g9, kw9), (g4, {})) * 2]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
