@@ -2,7 +2,7 @@
 random star surfaces, eps1/eps2 (including eps2 < eps1 and eps2 ~ eps1),
 kappa from 0 through 1e-12 to 5, vectors with a zero phi or dphi block,
 HOBI and LOBI; matvec, RHS and energy relative errors per case.
-Usage: python tools/fuzz_parity.py [n_cases]"""
+Usage: python tests/checks/fuzz_parity.py [n_cases]"""
 import sys
 import numpy as np
 sys.path.insert(0, '.'); sys.path.insert(0, 'oracle')

@@ -1,7 +1,7 @@
 """Index-arithmetic check beyond the BASELINE sizes: config 5's surface at a
 finer icosphere level (default 8: 1,310,720 triangles, 5.2M regular points,
 3.4e12 pairs per matvec).  Full GPU matvec, then sampled row blocks against the
-oracle's _apply_range restatement.  Usage: python tools/scale_rows_check.py [level]"""
+oracle's _apply_range restatement.  Usage: python tests/checks/scale_rows_check.py [level]"""
 import sys, time
 import numpy as np
 sys.path.insert(0, '.'); sys.path.insert(0, 'oracle')
