@@ -167,14 +167,31 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
       const int st = (int)(pos % kStages);
       mbar_wait(&bars[st], (pos / kStages) & 1u);
       const double2* rec = reinterpret_cast<const double2*>(ring + st * kSrcTile * kSrcStride);
+      // LOBI: only source tiles overlapping this item's target rows hold a
+      // self pair; every other tile takes the unmasked step-major path
+      // (uniform per CTA).  Both paths give bitwise the same sums.
+      bool fast = STEP;
+      if constexpr (STEP && SELF) {
+        const int64_t s0 = (int64_t)(tile0 + it) * kSrcTile;
+        const int64_t tlo = t_begin + (int64_t)tt * kTile;
+        fast = !(s0 < tlo + kTile && s0 + kSrcTile > tlo);
+      }
+      if constexpr (STEP) {
+        if (fast) {
 #pragma unroll UNROLL
-      for (int j = 0; j < (warp_live ? kSrcTile : 0); ++j) {
-        const double2 p01 = rec[5 * j + 0], p2m0 = rec[5 * j + 1], m12 = rec[5 * j + 2];
-        const double2 w01 = rec[5 * j + 3], w2x = rec[5 * j + 4];
-        if constexpr (STEP) {
-          pairs_screened_stepmajor<R>(tx, ty, tz, nx, ny, nz, p01.x, p01.y, p2m0.x, p2m0.y, m12.x,
-                                      m12.y, w01.x, w01.y, w2x.x, Ap, Bp, etab, a1, a2);
-        } else {
+          for (int j = 0; j < (warp_live ? kSrcTile : 0); ++j) {
+            const double2 p01 = rec[5 * j + 0], p2m0 = rec[5 * j + 1], m12 = rec[5 * j + 2];
+            const double2 w01 = rec[5 * j + 3], w2x = rec[5 * j + 4];
+            pairs_screened_stepmajor<R>(tx, ty, tz, nx, ny, nz, p01.x, p01.y, p2m0.x, p2m0.y, m12.x,
+                                        m12.y, w01.x, w01.y, w2x.x, Ap, Bp, etab, a1, a2);
+          }
+        }
+      }
+      if (!fast) {
+#pragma unroll UNROLL
+        for (int j = 0; j < (warp_live ? kSrcTile : 0); ++j) {
+          const double2 p01 = rec[5 * j + 0], p2m0 = rec[5 * j + 1], m12 = rec[5 * j + 2];
+          const double2 w01 = rec[5 * j + 3], w2x = rec[5 * j + 4];
 #pragma unroll
           for (int q = 0; q < R; ++q) {
             double sx = p01.x, sy = p01.y, sz = p2m0.x;
@@ -198,7 +215,7 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
               pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, mx, my, mz, D,
                                  a1[q], a2[q]);
           }
-        }  // STEP
+        }
       }
       __syncthreads();
     }
@@ -515,6 +532,12 @@ static const SweepVariant kVariants[] = {
 #undef HOBI_V
 #undef HOBI_VS
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+// LOBI (self-pair mask) counterparts of the wide / narrow / small tiles.
+static const SweepVariant kSelfVariants[] = {
+    {sweep_kernel<kScreened, true, true, 6, 2, 2, true>, 6, "self_step_R6_minb2_unroll2"},
+    {sweep_kernel<kScreened, true, true, 4, 3, 2, true>, 4, "self_step_R4_minb3_unroll2"},
+    {sweep_kernel<kScreened, true, true, 1, 6, 2>, 1, "self_R1_minb6_unroll2"},
+};
 constexpr int kSmallVariant = 3;   // R1_minb8_unroll2
 constexpr int kWideVariant = 17;   // step_R6_minb2_unroll2: 768-row tiles, the default
 constexpr int kNarrowVariant = 15; // step_R4_minb3_unroll2: 512-row tiles
@@ -565,30 +588,33 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
   int nseg = 1;
   seg[0] = {nullptr, kSweepR, t0, t1};
   if (c->phys.mode == kScreened) {
-    if (self)
-      seg[0].fn = sweep_kernel<kScreened, true, true, kSweepR, 1, 2>;
-    else if (full) {
-      int vi = c->sweep_variant;
+    if (full) {
+      // LOBI runs the same tile choice on the self-masked instantiations
+      const SweepVariant* tab = self ? kSelfVariants : kVariants;
+      const int wide = self ? 0 : kWideVariant, narrow = self ? 1 : kNarrowVariant,
+                small = self ? 2 : kSmallVariant;
+      int vi = self ? wide : c->sweep_variant;
+      const bool pinned = c->variant_pinned && !self;
       // the wide tile is ~1% faster per pair, but a range that leaves more
       // than 2% of its rows past the last whole 768-row tile (an 8-way split
       // of config 4 leaves 513 of 5121) runs better on 512-row tiles
-      if (!c->variant_pinned && vi == kWideVariant) {
+      if (!pinned && vi == wide) {
         const int64_t rows = t1 - t0;
-        const int64_t rem_w = rows % (kSweepThreads * kVariants[kWideVariant].r);
-        const int64_t rem_n = rows % (kSweepThreads * kVariants[kNarrowVariant].r);
-        if (rem_w * 50 > rows && rem_n < rem_w) vi = kNarrowVariant;
+        const int64_t rem_w = rows % (kSweepThreads * tab[wide].r);
+        const int64_t rem_n = rows % (kSweepThreads * tab[narrow].r);
+        if (rem_w * 50 > rows && rem_n < rem_w) vi = narrow;
       }
       // small problems: if the tuned tile leaves too few work items for 148
       // SMs, use 128-row tiles (same sums bitwise, more parallelism)
-      const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * kVariants[vi].r) * n_groups;
-      if (!c->variant_pinned && items < 8 * 296) vi = kSmallVariant;
-      seg[0].fn = kVariants[vi].fn;
-      seg[0].r = kVariants[vi].r;
+      const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * tab[vi].r) * n_groups;
+      if (!pinned && items < 8 * 296) vi = small;
+      seg[0].fn = tab[vi].fn;
+      seg[0].r = tab[vi].r;
       const int64_t tile = (int64_t)kSweepThreads * seg[0].r;
       const int64_t whole = (t1 - t0) / tile * tile;
-      if (!c->variant_pinned && seg[0].r > 1 && whole > 0 && whole < t1 - t0) {
+      if (!pinned && seg[0].r > 1 && whole > 0 && whole < t1 - t0) {
         seg[0].b = t0 + whole;
-        seg[1] = {kVariants[kSmallVariant].fn, kVariants[kSmallVariant].r, t0 + whole, t1};
+        seg[1] = {tab[small].fn, tab[small].r, t0 + whole, t1};
         nseg = 2;
       }
     } else
