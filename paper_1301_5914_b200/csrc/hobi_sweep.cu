@@ -168,14 +168,16 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
       mbar_wait(&bars[st], (pos / kStages) & 1u);
       const double2* rec = reinterpret_cast<const double2*>(ring + st * kSrcTile * kSrcStride);
       // LOBI: only source tiles overlapping this item's target rows hold a
-      // self pair; every other tile takes the unmasked step-major path
-      // (uniform per CTA).  Both paths give bitwise the same sums.
-      bool fast = STEP;
-      if constexpr (STEP && SELF) {
+      // self pair; every other tile takes the unmasked path (step-major where
+      // the instantiation has one), a branch uniform per CTA.  Both paths give
+      // bitwise the same sums.
+      bool masked = false;
+      if constexpr (SELF) {
         const int64_t s0 = (int64_t)(tile0 + it) * kSrcTile;
         const int64_t tlo = t_begin + (int64_t)tt * kTile;
-        fast = !(s0 < tlo + kTile && s0 + kSrcTile > tlo);
+        masked = s0 < tlo + kTile && s0 + kSrcTile > tlo;
       }
+      const bool fast = STEP && !masked;
       if constexpr (STEP) {
         if (fast) {
 #pragma unroll UNROLL
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
           for (int q = 0; q < R; ++q) {
             double sx = p01.x, sy = p01.y, sz = p2m0.x;
             double mx = p2m0.y, my = m12.x, mz = m12.y, W1 = w01.x, C = w01.y, D = w2x.x;
-            if (SELF) {
+            if (SELF && masked) {
               // LOBI self pair: displacement forced to (1,0,0) and every weight
               // (the weighted normal included) to 0, so it contributes exactly +0
               // (solver.py:303-310).
@@ -538,6 +540,18 @@ static const SweepVariant kSelfVariants[] = {
     {sweep_kernel<kScreened, true, true, 4, 3, 2, true>, 4, "self_step_R4_minb3_unroll2"},
     {sweep_kernel<kScreened, true, true, 1, 6, 2>, 1, "self_R1_minb6_unroll2"},
 };
+// kappa = 0 (Laplace instantiation, no step-major form needed): wide / narrow
+// / small tiles, without and with the LOBI self mask.
+static const SweepVariant kLaplaceVariants[] = {
+    {sweep_kernel<kLaplace, true, false, 6, 2, 2>, 6, "laplace_R6_minb2_unroll2"},
+    {sweep_kernel<kLaplace, true, false, 4, 3, 2>, 4, "laplace_R4_minb3_unroll2"},
+    {sweep_kernel<kLaplace, true, false, 1, 8, 2>, 1, "laplace_R1_minb8_unroll2"},
+};
+static const SweepVariant kLaplaceSelfVariants[] = {
+    {sweep_kernel<kLaplace, true, true, 6, 2, 2>, 6, "laplace_self_R6_minb2_unroll2"},
+    {sweep_kernel<kLaplace, true, true, 4, 3, 2>, 4, "laplace_self_R4_minb3_unroll2"},
+    {sweep_kernel<kLaplace, true, true, 1, 6, 2>, 1, "laplace_self_R1_minb6_unroll2"},
+};
 constexpr int kSmallVariant = 3;   // R1_minb8_unroll2
 constexpr int kWideVariant = 17;   // step_R6_minb2_unroll2: 768-row tiles, the default
 constexpr int kNarrowVariant = 15; // step_R4_minb3_unroll2: 512-row tiles
@@ -587,14 +601,18 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
   } seg[2];
   int nseg = 1;
   seg[0] = {nullptr, kSweepR, t0, t1};
-  if (c->phys.mode == kScreened) {
-    if (full) {
-      // LOBI runs the same tile choice on the self-masked instantiations
-      const SweepVariant* tab = self ? kSelfVariants : kVariants;
-      const int wide = self ? 0 : kWideVariant, narrow = self ? 1 : kNarrowVariant,
-                small = self ? 2 : kSmallVariant;
-      int vi = self ? wide : c->sweep_variant;
-      const bool pinned = c->variant_pinned && !self;
+  if (full) {
+    {
+      // the tuning table for screened HOBI; LOBI (self mask) and kappa = 0 run
+      // the same tile choice on their own wide / narrow / small instantiations
+      const bool tuned = c->phys.mode == kScreened && !self;
+      const SweepVariant* tab = tuned ? kVariants
+                                : c->phys.mode == kScreened ? kSelfVariants
+                                : self ? kLaplaceSelfVariants : kLaplaceVariants;
+      const int wide = tuned ? kWideVariant : 0, narrow = tuned ? kNarrowVariant : 1,
+                small = tuned ? kSmallVariant : 2;
+      int vi = tuned ? c->sweep_variant : wide;
+      const bool pinned = c->variant_pinned && tuned;
       // the wide tile is ~1% faster per pair, but a range that leaves more
       // than 2% of its rows past the last whole 768-row tile (an 8-way split
       // of config 4 leaves 513 of 5121) runs better on 512-row tiles
@@ -617,12 +635,10 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
         seg[1] = {tab[small].fn, tab[small].r, t0 + whole, t1};
         nseg = 2;
       }
-    } else
-      seg[0].fn = sweep_kernel<kScreened, false, false, kSweepR, 1, 2>;
-  } else {
-    seg[0].fn = self ? sweep_kernel<kLaplace, true, true, kSweepR, 1, 2>
-                     : (full ? sweep_kernel<kLaplace, true, false, kSweepR, 1, 2>
-                             : sweep_kernel<kLaplace, false, false, kSweepR, 1, 2>);
+    }
+  } else {  // energy: K1/K2 only, charges as targets
+    seg[0].fn = c->phys.mode == kScreened ? sweep_kernel<kScreened, false, false, kSweepR, 1, 2>
+                                          : sweep_kernel<kLaplace, false, false, kSweepR, 1, 2>;
   }
   if (!c->sms) HOBI_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
   const int sms = c->sms;

@@ -1,0 +1,20 @@
+"""Sweep throughput at kappa = 0 (Laplace instantiation) vs screened, config-4 surface."""
+import sys, ctypes as C, numpy as np
+sys.path.insert(0, '.')
+from paper_1301_5914_b200 import _native as N, discretize, PhysicalParams, SolverConfig, matvec_hobi, matvec_lobi
+from paper_1301_5914_b200.surfaces import baseline_config
+lib = N.load()
+cfg = baseline_config(4)
+for kap in (0.0, cfg.kappa):
+    for scheme, mv in (("hobi", matvec_hobi), ("lobi", matvec_lobi)):
+        prob = discretize(cfg.mesh, PhysicalParams(cfg.eps1, cfg.eps2, kap), cfg.charges, SolverConfig(scheme=scheme, workers=1))
+        u = np.random.default_rng(0).standard_normal(prob.n_unknowns)
+        mv(prob, u)
+        lib.hobi_timing_reset(prob.handle)
+        for _ in range(4): mv(prob, u)
+        ms = C.c_double(0); nl = C.c_int64(0)
+        lib.hobi_timing(prob.handle, C.byref(ms), C.byref(nl), None)
+        pairs = C.c_double(0); lib.hobi_pairs_per_matvec(prob.handle, C.byref(pairs))
+        t = ms.value / 4
+        print(f"kappa={kap:g} {scheme}: {t:.3f} ms per sweep, {pairs.value/t*1e3:.3e} pairs/s", flush=True)
+        prob.close()
