@@ -170,6 +170,25 @@ int hobi_comm_init(hobi_ctx* ctx, const unsigned char id[128], int nranks, int r
  */
 int hobi_comm_p2p_handle(hobi_ctx* ctx, unsigned char handle[64]);
 int hobi_comm_p2p_open(hobi_ctx* ctx, const unsigned char* handles, int nranks, int rank);
+
+/*
+ * Single-process multi-GPU group (SolverConfig.workers -> GPUs without
+ * torchrun; replaces the fork pool of solver.py:405-477 inside one process).
+ * `members` are contexts of the same problem, usually one per device
+ * (member 0 leads: inputs, outputs and GMRES live there); member i owns rows
+ * partition_targets(n_colloc, size)[i].  Each application copies the iterate
+ * peer-to-peer to the members, runs every member's rows on its own device and
+ * copies them back; devices are ordered by events only, so members may also
+ * share a device.  Results are bitwise those of one context.  Members must
+ * outlive every group call and must not be in a communicator or emulated
+ * split; hobi_group_destroy touches only the group's own buffers.
+ */
+typedef struct hobi_group hobi_group;
+int hobi_group_create(hobi_ctx* const* members, int size, hobi_group** out);
+int hobi_group_destroy(hobi_group* group);
+int hobi_group_matvec(hobi_group* group, const double* u, double* out);
+int hobi_group_gmres(hobi_group* group, const double* b, double tol, int restart, int max_it, double* x,
+                     int* iterations, double* residual, double* best, int* matvecs);
 /* Single-GPU emulation of an nranks-way split (same buffers, same gather
  * layout and permutation kernel, no NCCL): for determinism tests. */
 int hobi_emulate_ranks(hobi_ctx* ctx, int nranks);

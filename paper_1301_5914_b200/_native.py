@@ -52,6 +52,11 @@ SIGNATURES = {
     "hobi_gmres_host_operator": (C.c_int, [C.c_int, C.c_int64, APPLY_FN, C.c_void_p, _dp, C.c_double,
                                            C.c_int, C.c_int, _dp, C.POINTER(C.c_int), _dp, _dp,
                                            C.POINTER(C.c_int)]),
+    "hobi_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p)]),
+    "hobi_group_destroy": (C.c_int, [C.c_void_p]),
+    "hobi_group_matvec": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "hobi_group_gmres": (C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, C.c_int, _dp, C.POINTER(C.c_int),
+                                   _dp, _dp, C.POINTER(C.c_int)]),
     "hobi_export_caches": (C.c_int, [_ctxp, _dp, _dp, _dp, _dp, _dp, _dp, _i64p, _i64p, _i64p, _i64p]),
     "hobi_export_nodes": (C.c_int, [_ctxp, _dp, _dp]),
     "hobi_kernel_values": (C.c_int, [C.c_int, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_double,

@@ -25,6 +25,7 @@ UNITS = {
     "hobi_api.cu": [],
     "hobi_sweep.cu": [],
     "hobi_gmres.cu": [],
+    "hobi_group.cu": [],
     "hobi_geometry.cu": ["-fmad=false"],
     "hobi_literal.cu": ["-fmad=false"],
 }

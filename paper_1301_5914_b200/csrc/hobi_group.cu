@@ -1,0 +1,184 @@
+// Single-process multi-GPU operator (SolverConfig.workers -> GPUs, the
+// reference's fork-pool row split, solver.py:405-477, without torchrun).
+//
+// A group holds one context per device, each with the full caches
+// (replicated, as in the one-process-per-GPU mode).  Member i owns rows
+// partition_targets(n, size)[i].  One application: the leader's input is
+// copied peer-to-peer to every member (NVLink on an NVSwitch box), each member
+// runs the sweep + epilogue of its rows on its own streams, copies its [2][m]
+// slot back into the leader's rank-major receive buffer, and the leader waits
+// on every member's event and permutes.  Only event waits order the devices --
+// no kernel waits on another -- so members may share a device (that is how
+// the path is tested on one GPU).  Rows are bitwise identical for any split,
+// so a group solve equals the one-GPU solve bit for bit.  GMRES runs on the
+// leader through the same device-resident solver.
+#include <algorithm>
+#include <vector>
+
+#include "hobi_internal.cuh"
+
+namespace hobi {
+namespace {
+
+struct Member {
+  hobi_ctx* c = nullptr;
+  int device = 0;  // kept so the group can be released after its members
+  int64_t lo = 0, hi = 0;
+  DevBuf<double> u, slot;  // input copy and [2][m] output slot on the member's device
+  cudaEvent_t done = nullptr;
+};
+
+}  // namespace
+}  // namespace hobi
+
+struct hobi_group {
+  std::vector<hobi::Member> m;
+  int64_t nt = 0, slot_m = 0;
+  hobi::DevBuf<double> recv;  // leader: [size][2][slot_m]
+  cudaEvent_t in_ready = nullptr, gathered = nullptr;
+  hobi::GmresWorkspace gmres_ws;
+};
+
+using namespace hobi;
+
+namespace {
+
+struct GroupOperator : DeviceOperator {
+  hobi_group* g;
+  explicit GroupOperator(hobi_group* grp) : g(grp) {}
+  int apply(const double* in, double* out) override {
+    hobi_ctx* lead = g->m[0].c;
+    const size_t bytes = 2 * g->nt * sizeof(double);
+    HOBI_CUDA(cudaSetDevice(lead->device));
+    HOBI_CUDA(cudaEventRecord(g->in_ready, lead->stream));
+    for (size_t i = 0; i < g->m.size(); ++i) {
+      Member& mb = g->m[i];
+      hobi_ctx* c = mb.c;
+      HOBI_CUDA(cudaSetDevice(c->device));
+      HOBI_CUDA(cudaStreamWaitEvent(c->stream, g->in_ready, 0));
+      const double* u = in;
+      if (i > 0) {  // peer copy of the iterate (NVLink), then the member's own rows
+        HOBI_CUDA(cudaMemcpyPeerAsync(mb.u.p, c->device, in, lead->device, bytes, c->stream));
+        u = mb.u.p;
+      }
+      int rc = matvec_rows_device(c, u, mb.lo, mb.hi, mb.slot.p, mb.slot.p + g->slot_m);
+      if (rc) return rc;
+      HOBI_CUDA(cudaMemcpyPeerAsync(g->recv.p + i * 2 * g->slot_m, lead->device, mb.slot.p, c->device,
+                                    2 * g->slot_m * sizeof(double), c->stream));
+      HOBI_CUDA(cudaEventRecord(mb.done, c->stream));
+    }
+    HOBI_CUDA(cudaSetDevice(lead->device));
+    for (Member& mb : g->m) HOBI_CUDA(cudaStreamWaitEvent(lead->stream, mb.done, 0));
+    int rc = permute_rows(lead->stream, g->recv.p, g->slot_m, g->nt, (int)g->m.size(), out);
+    lead->launches++;
+    return rc;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int hobi_group_create(hobi_ctx* const* members, int size, hobi_group** out) {
+  *out = nullptr;
+  if (size < 1 || !members) return fail(HOBI_ERR_VALUE, "a group needs at least one context");
+  for (int i = 0; i < size; ++i) {
+    const hobi_ctx* c = members[i];
+    if (!c) return fail(HOBI_ERR_STATE, "null context in group");
+    const hobi_ctx* l = members[0];
+    if (c->nt != l->nt || c->ns != l->ns || c->scheme != l->scheme || c->nq != l->nq)
+      return fail(HOBI_ERR_VALUE, "group members must discretise the same problem");
+    if (c->comm.nranks != 1 || c->comm.emulated)
+      return fail(HOBI_ERR_STATE, "group members must not be in a communicator or emulated split");
+  }
+  hobi_group* g = new hobi_group();
+  auto bail = [&](int rc) {
+    hobi_group_destroy(g);
+    return rc;
+  };
+  g->nt = members[0]->nt;
+  g->slot_m = std::max<int64_t>(1, (g->nt + size - 1) / size);
+  g->m.resize(size);
+  for (int i = 0; i < size; ++i) {
+    Member& mb = g->m[i];
+    mb.c = members[i];
+    mb.device = mb.c->device;
+    const int64_t base = g->nt / size, extra = g->nt % size;
+    mb.lo = i * base + std::min<int64_t>(i, extra);
+    mb.hi = mb.lo + base + (i < extra ? 1 : 0);
+    if (cudaSetDevice(mb.c->device) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "cudaSetDevice"));
+    if (mb.u.alloc(2 * g->nt) || mb.slot.alloc(2 * g->slot_m)) return bail(HOBI_ERR_CUDA);
+    cudaError_t e = cudaEventCreateWithFlags(&mb.done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
+  }
+  hobi_ctx* lead = members[0];
+  if (cudaSetDevice(lead->device) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "cudaSetDevice"));
+  if (g->recv.alloc((size_t)size * 2 * g->slot_m)) return bail(HOBI_ERR_CUDA);
+  cudaError_t e = cudaEventCreateWithFlags(&g->in_ready, cudaEventDisableTiming);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
+  // peer access between distinct devices (NVLink); same-device members need none
+  for (int i = 1; i < size; ++i) {
+    const int d = members[i]->device;
+    if (d == lead->device) continue;
+    int ok = 0;
+    cudaDeviceCanAccessPeer(&ok, lead->device, d);
+    if (ok) {
+      cudaSetDevice(lead->device);
+      e = cudaDeviceEnablePeerAccess(d, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return bail(cuda_fail(e, "peer access"));
+      cudaSetDevice(d);
+      e = cudaDeviceEnablePeerAccess(lead->device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return bail(cuda_fail(e, "peer access"));
+      cudaGetLastError();  // clear a tolerated "already enabled"
+    }
+  }
+  *out = g;
+  return 0;
+}
+
+// Touches only the group's own resources (never the member contexts), so it
+// is safe after the members are gone.
+int hobi_group_destroy(hobi_group* g) {
+  if (!g) return 0;
+  for (Member& mb : g->m) {
+    if (!mb.c) continue;
+    cudaSetDevice(mb.device);
+    cudaDeviceSynchronize();
+    if (mb.done) cudaEventDestroy(mb.done);
+    mb.u.release();
+    mb.slot.release();
+  }
+  if (!g->m.empty()) cudaSetDevice(g->m[0].device);
+  if (g->in_ready) cudaEventDestroy(g->in_ready);
+  delete g;  // leader-device buffers free themselves (leader is current)
+  return 0;
+}
+
+int hobi_group_matvec(hobi_group* g, const double* u, double* out) {
+  if (!g) return fail(HOBI_ERR_STATE, "null group");
+  hobi_ctx* lead = g->m[0].c;
+  HOBI_CUDA(cudaSetDevice(lead->device));
+  const size_t bytes = 2 * g->nt * sizeof(double);
+  HOBI_CUDA(cudaMemcpyAsync(lead->u.p, u, bytes, cudaMemcpyHostToDevice, lead->stream));
+  GroupOperator op(g);
+  int rc = op.apply(lead->u.p, lead->out.p);
+  if (rc) return rc;
+  HOBI_CUDA(cudaSetDevice(lead->device));
+  HOBI_CUDA(cudaMemcpyAsync(out, lead->out.p, bytes, cudaMemcpyDeviceToHost, lead->stream));
+  HOBI_CUDA(cudaStreamSynchronize(lead->stream));
+  return 0;
+}
+
+int hobi_group_gmres(hobi_group* g, const double* b, double tol, int restart, int max_it, double* x,
+                     int* iterations, double* residual, double* best, int* matvecs) {
+  if (!g) return fail(HOBI_ERR_STATE, "null group");
+  hobi_ctx* lead = g->m[0].c;
+  HOBI_CUDA(cudaSetDevice(lead->device));
+  GroupOperator op(g);
+  int rc = gmres_device(lead->device, lead->stream, 2 * g->nt, &op, b, tol, restart, max_it, x, iterations,
+                        residual, best, matvecs, &lead->launches, &g->gmres_ws);
+  cudaSetDevice(lead->device);
+  return rc;
+}
+
+}  // extern "C"

@@ -179,6 +179,7 @@ class DiscretizedProblem:
         self._duffy = duffy
         self._cache = {}
         self.rank, self.world = rank_info
+        self.device = _device_index()
         x = mesh.vertices[mesh.faces]
         cr = np.cross(x[:, 1] - x[:, 0], x[:, 2] - x[:, 0])
         two = np.linalg.norm(cr, axis=1)
@@ -261,18 +262,12 @@ class DiscretizedProblem:
         return self.pair_face[lo:hi]
 
 
-def discretize(mesh: FlatMesh, params: PhysicalParams, charges: ChargeSystem,
-               config: SolverConfig) -> DiscretizedProblem:
-    """Validate the mesh and build every cache on the GPU (solver.py:165-266)."""
-    mesh.validate()
-    N.require_device()
+def _create_handle(mesh: FlatMesh, params: PhysicalParams, scheme: str, rule, duffy, dev: int) -> "_Handle":
+    """One native context of the problem on device `dev`."""
     lib = N.load()
-    dev = _device_index()
     v, n, f = N.f64(mesh.vertices), N.f64(mesh.normals), N.i64(mesh.faces)
     ctx = C.c_void_p()
-    rule = config.regular_rule
-    duffy = duffy_rule(config.duffy_points)
-    if config.scheme == "hobi":
+    if scheme == "hobi":
         rpts, rw, rsh = N.f64(rule.points), N.f64(rule.weights), N.f64(shape_tables(rule.points))
         dpts, dw, dsh = N.f64(duffy.points), N.f64(duffy.weights), N.f64(shape_tables(duffy.points))
         st = lib.hobi_create(dev, N.dptr(v), N.dptr(n), mesh.n_vertices, N.iptr(f), mesh.n_faces,
@@ -283,7 +278,18 @@ def discretize(mesh: FlatMesh, params: PhysicalParams, charges: ChargeSystem,
         st = lib.hobi_create_lobi(dev, N.dptr(v), N.dptr(n), mesh.n_vertices, N.iptr(f), mesh.n_faces,
                                   params.eps1, params.eps2, params.kappa, C.byref(ctx))
     _raise(st)
-    handle = _Handle(ctx.value)
+    return _Handle(ctx.value)
+
+
+def discretize(mesh: FlatMesh, params: PhysicalParams, charges: ChargeSystem,
+               config: SolverConfig) -> DiscretizedProblem:
+    """Validate the mesh and build every cache on the GPU (solver.py:165-266)."""
+    mesh.validate()
+    N.require_device()
+    dev = _device_index()
+    rule = config.regular_rule
+    duffy = duffy_rule(config.duffy_points)
+    handle = _create_handle(mesh, params, config.scheme, rule, duffy, dev)
     rank, world, _ = _world()
     # HOBI_FORCE_NCCL=1 runs the collective path even for a one-rank job (test hook)
     if world > 1 or (_dist_initialized() and os.environ.get("HOBI_FORCE_NCCL") == "1"):
@@ -411,30 +417,73 @@ def partition_targets(n_targets: int, n_workers: int) -> list[tuple[int, int]]:
 class GpuOperator:
     """Callable matvec with the reference operator protocol (solver.py:432-472).
 
-    ``workers`` > 1 in a single process emulates that many row partitions on
-    one GPU (same gather layout and permutation kernel as the NCCL path).
+    ``workers`` > 1 is the reference's row split (solver.py:405-477).  In a
+    single process with at least ``workers`` visible GPUs the rows run on that
+    many GPUs (``devices``, default 0..workers-1 with the problem's device
+    first): every extra device gets a replica context and the native group
+    operator gathers the rows over peer copies.  With fewer GPUs the split is
+    emulated on the problem's GPU (same gather layout and permutation as the
+    NCCL path).  Either way the result is bitwise that of one GPU.
+    ``devices`` may repeat a device (replicas sharing it) -- the test hook for
+    the group path on a one-GPU machine.
     """
 
-    def __init__(self, problem: DiscretizedProblem, workers: int = 1):
+    def __init__(self, problem: DiscretizedProblem, workers: int = 1, devices=None):
         self._problem = problem
         self._closed = False
-        if problem.world == 1 and workers > 1 and problem.n_collocation > 0:
-            _raise(N.load().hobi_emulate_ranks(problem.handle, workers))
+        self._emulated = False
+        self._group = None
+        self._replicas = []
+        lib = N.load()
+        if problem.world != 1 or problem.n_collocation == 0:
+            return
+        if devices is None and workers > 1 and N.device_count() >= workers:
+            others = [d for d in range(N.device_count()) if d != problem.device]
+            devices = [problem.device] + others[: workers - 1]
+        if devices is not None and len(devices) > 1:
+            devices = list(devices)
+            if devices[0] != problem.device:
+                raise ValueError(f"devices[0] must be the problem's device {problem.device}")
+            for d in devices[1:]:
+                self._replicas.append(_create_handle(problem.mesh, problem.params, problem.scheme,
+                                                     problem._rule, problem._duffy, int(d)))
+            members = (C.c_void_p * len(devices))(problem.handle, *[h.ptr for h in self._replicas])
+            grp = C.c_void_p()
+            _raise(lib.hobi_group_create(members, len(devices), C.byref(grp)))
+            self._group = grp.value
+        elif workers > 1:
+            _raise(lib.hobi_emulate_ranks(problem.handle, workers))
             self._emulated = True
-        else:
-            self._emulated = False
 
     @property
     def problem(self):
         return self._problem
 
+    @property
+    def group(self):
+        """Native multi-GPU group handle, or None."""
+        return self._group
+
     def __call__(self, u) -> np.ndarray:
         if self._closed:
             raise ValueError("operator is closed")
-        return _full_matvec(self._problem, u)
+        if self._group is None:
+            return _full_matvec(self._problem, u)
+        u = _as_vector(self._problem, u)
+        out = np.empty_like(u)
+        _raise(N.load().hobi_group_matvec(self._group, N.dptr(u), N.dptr(out)))
+        return out
 
     def close(self):
-        if self._emulated and not self._closed:
+        if self._closed:
+            return
+        if self._group is not None:
+            N.load().hobi_group_destroy(self._group)
+            self._group = None
+        for h in self._replicas:
+            h.__del__()
+        self._replicas = []
+        if self._emulated:
             _raise(N.load().hobi_emulate_ranks(self._problem.handle, 1))
         self._closed = True
 
@@ -443,6 +492,12 @@ class GpuOperator:
 
     def __exit__(self, *exc):
         self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def make_operator(problem: DiscretizedProblem, config: SolverConfig) -> GpuOperator:
@@ -465,7 +520,11 @@ def gmres_solve(apply, b, config: SolverConfig) -> SurfaceSolution:
     x = np.empty(n)
     its, mv = C.c_int(0), C.c_int(0)
     res, best = C.c_double(0.0), C.c_double(0.0)
-    if isinstance(apply, GpuOperator):
+    if isinstance(apply, GpuOperator) and apply.group is not None:
+        st = lib.hobi_group_gmres(apply.group, N.dptr(b), config.tolerance, config.restart,
+                                  config.max_iterations, N.dptr(x), C.byref(its), C.byref(res),
+                                  C.byref(best), C.byref(mv))
+    elif isinstance(apply, GpuOperator):
         st = lib.hobi_gmres(apply.problem.handle, N.dptr(b), config.tolerance, config.restart,
                             config.max_iterations, N.dptr(x), C.byref(its), C.byref(res), C.byref(best),
                             C.byref(mv))

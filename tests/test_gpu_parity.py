@@ -553,3 +553,33 @@ def test_lobi_self_mask_tiles_bitwise_across_splits():
     u4 = np.random.default_rng(24).standard_normal(p4.n_unknowns)
     assert rel_l2(matvec_lobi(p4, u4), O.matvec(o4, u4)) <= MATVEC_TOL
     p4.close()
+
+
+@pytest.mark.parametrize("scheme", ["hobi", "lobi"])
+def test_single_process_group_operator_bitwise(scheme):
+    """The single-process multi-GPU group (workers -> GPUs without torchrun):
+    replicas on the problem's device stand in for peers (copies between
+    members are ordered by events only, so sharing a device is legal).  The
+    group matvec and the group GMRES solve are bitwise those of one context."""
+    from paper_1301_5914_b200.solver import GpuOperator
+
+    g = golden("star_l3")
+    prob = _problem(g, scheme=scheme)
+    cfg = SolverConfig(workers=1, restart=int(g["restart"]), scheme=scheme)
+    u = np.random.default_rng(31).standard_normal(prob.n_unknowns)
+    mv = matvec_hobi if scheme == "hobi" else matvec_lobi
+    ref = mv(prob, u)
+    b = assemble_rhs(prob)
+    with make_operator(prob, cfg) as op:
+        sol_ref = gmres_solve(op, b, cfg)
+    dev = prob.device
+    for devices in ([dev, dev], [dev, dev, dev]):
+        with GpuOperator(prob, len(devices), devices=devices) as op:
+            assert op.group is not None
+            assert np.array_equal(op(u), ref), devices
+            sol = gmres_solve(op, b, cfg)
+        assert sol.iterations == sol_ref.iterations and np.array_equal(sol.vector, sol_ref.vector)
+    assert np.array_equal(mv(prob, u), ref)  # the problem itself is untouched
+    op = GpuOperator(prob, 2, devices=[dev, dev])
+    prob.close()
+    op.close()  # releasing the group after its leader is gone is safe
