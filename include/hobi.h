@@ -124,6 +124,17 @@ int hobi_gmres(hobi_ctx* ctx, const double* b, double tol, int restart, int max_
                int* iterations, double* residual, double* best, int* matvecs);
 
 /*
+ * solve() after discretize (solver.py:563-574) in one call, for C/C++
+ * integrators: RHS, GMRES to `tol`, then the energy.  phi and dphi receive
+ * n_colloc entries each; iterations/residual/matvecs as hobi_gmres.  Status
+ * codes as the three calls it chains (a non-converged solve returns
+ * HOBI_ERR_NONCONVERGENCE; phi, dphi and energy are then unspecified).
+ */
+int hobi_solve(hobi_ctx* ctx, const double* qpos, const double* q, int64_t nc, double tol, int restart,
+               int max_it, double* phi, double* dphi, double* energy, int* iterations, double* residual,
+               int* matvecs);
+
+/*
  * The same GMRES on an arbitrary operator supplied as a host callback
  * (gmres_solve accepts any callable, solver.py:484).  `apply` receives host
  * arrays of length n and returns 0 on success.

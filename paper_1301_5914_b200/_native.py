@@ -49,6 +49,8 @@ SIGNATURES = {
     "hobi_energy": (C.c_int, [_ctxp, _dp, _dp, C.c_int64, _dp, _dp, _dp]),
     "hobi_gmres": (C.c_int, [_ctxp, _dp, C.c_double, C.c_int, C.c_int, _dp, C.POINTER(C.c_int), _dp, _dp,
                              C.POINTER(C.c_int)]),
+    "hobi_solve": (C.c_int, [_ctxp, _dp, _dp, C.c_int64, C.c_double, C.c_int, C.c_int, _dp, _dp, _dp,
+                             C.POINTER(C.c_int), _dp, C.POINTER(C.c_int)]),
     "hobi_gmres_host_operator": (C.c_int, [C.c_int, C.c_int64, APPLY_FN, C.c_void_p, _dp, C.c_double,
                                            C.c_int, C.c_int, _dp, C.POINTER(C.c_int), _dp, _dp,
                                            C.POINTER(C.c_int)]),

@@ -604,6 +604,23 @@ int hobi_gmres(hobi_ctx* c, const double* b, double tol, int restart, int max_it
   return rc2 ? rc2 : rc;
 }
 
+int hobi_solve(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, double tol, int restart,
+               int max_it, double* phi, double* dphi, double* energy, int* iterations, double* residual,
+               int* matvecs) {
+  NvtxRange nvtx_("hobi_solve");
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  *energy = 0.0;
+  std::vector<double> b(2 * c->nt), x(2 * c->nt);
+  int rc = hobi_rhs(c, qpos, q, nc, b.data());
+  if (rc) return rc;
+  double best = 0.0;
+  rc = hobi_gmres(c, b.data(), tol, restart, max_it, x.data(), iterations, residual, &best, matvecs);
+  std::copy(x.begin(), x.begin() + c->nt, phi);
+  std::copy(x.begin() + c->nt, x.end(), dphi);
+  if (rc) return rc;
+  return hobi_energy(c, qpos, q, nc, phi, dphi, energy);
+}
+
 int hobi_gmres_host_operator(int device, int64_t n, hobi_apply_fn apply, void* user, const double* b,
                              double tol, int restart, int max_it, double* x, int* iterations,
                              double* residual, double* best, int* matvecs) {

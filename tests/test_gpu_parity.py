@@ -583,3 +583,29 @@ def test_single_process_group_operator_bitwise(scheme):
     op = GpuOperator(prob, 2, devices=[dev, dev])
     prob.close()
     op.close()  # releasing the group after its leader is gone is safe
+
+
+def test_c_abi_one_call_solve_matches_python_path():
+    """hobi_solve (RHS + GMRES + energy in one C call, for C/C++ integrators)
+    equals the Python solve path bit for bit and the reference's golden."""
+    import ctypes as C
+
+    from paper_1301_5914_b200 import _native as N
+
+    g = golden("star_l2")
+    prob = _problem(g)
+    cfg = SolverConfig(workers=1, restart=int(g["restart"]))
+    with make_operator(prob, cfg) as op:
+        sol = gmres_solve(op, assemble_rhs(prob), cfg)
+    e_py = solvation_energy(prob, sol)
+    T = prob.n_collocation
+    phi, dphi, e = np.empty(T), np.empty(T), C.c_double(0)
+    its, res, mv = C.c_int(0), C.c_double(0), C.c_int(0)
+    q, qp = N.f64(g["q"]), N.f64(g["qpos"])
+    N.check(N.load().hobi_solve(prob.handle, N.dptr(qp), N.dptr(q), q.size, cfg.tolerance, cfg.restart,
+                                cfg.max_iterations, N.dptr(phi), N.dptr(dphi), C.byref(e), C.byref(its),
+                                C.byref(res), C.byref(mv)))
+    assert its.value == sol.iterations == int(g["iterations"]) and mv.value == sol.matvecs
+    assert np.array_equal(phi, sol.phi) and np.array_equal(dphi, sol.dphi_dn)
+    assert e.value == e_py
+    assert abs(e.value - float(g["energy"])) <= SOLVE_TOL * abs(float(g["energy"]))
