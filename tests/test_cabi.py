@@ -108,3 +108,25 @@ def test_public_api_covers_the_reference_surface():
         "partition_targets", "parse_msms", "radial_project", "solvation_energy", "solve",
         "surface_potential_error", "write_msms"]
     assert [n for n in reference_all if not hasattr(P, n)] == []
+
+
+def test_header_is_plain_c():
+    """include/hobi.h is a C header (no C++ or CUDA types cross the boundary):
+    it compiles as strict C99 and a C program can take every entry point."""
+    import shutil
+    import subprocess
+    import tempfile
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    names = _declared()
+    src = '#include "hobi.h"\ntypedef void (*fn_t)(void);\nint main(void) {\n  fn_t f;\n'
+    src += "".join(f"  f = (fn_t)&{n};\n  (void)f;\n" for n in names if n != "hobi_apply_fn")
+    src += "  return 0;\n}\n"
+    with tempfile.TemporaryDirectory() as tmp:
+        c_file = os.path.join(tmp, "probe.c")
+        open(c_file, "w").write(src)
+        out = subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-pedantic", "-fsyntax-only",
+                              "-I", os.path.join(ROOT, "include"), c_file], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
