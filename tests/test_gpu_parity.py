@@ -609,3 +609,39 @@ def test_c_abi_one_call_solve_matches_python_path():
     assert np.array_equal(phi, sol.phi) and np.array_equal(dphi, sol.dphi_dn)
     assert e.value == e_py
     assert abs(e.value - float(g["energy"])) <= SOLVE_TOL * abs(float(g["energy"]))
+
+
+def test_c_abi_argument_errors():
+    """Bad arguments come back as status codes with a message, never a crash:
+    out-of-range faces, oversized rules, kappa*extent beyond the table range,
+    group members of different problems, P2P open before its handle."""
+    import ctypes as C
+
+    from paper_1301_5914_b200 import _native as N
+
+    lib = N.load()
+    g = golden("star_l2")
+    v, n = N.f64(g["vertices"]), N.f64(g["normals"])
+    f = N.i64(g["faces"]).copy()
+    rule = np.zeros((1, 2)); w = np.ones(1); sh = np.zeros((3, 1, 10))
+    ctx = C.c_void_p()
+
+    def create(faces, nq=1, kappa=0.1):
+        return lib.hobi_create(0, N.dptr(v), N.dptr(n), v.shape[0], N.iptr(faces), faces.shape[0], 1.0, 80.0,
+                               kappa, N.dptr(N.f64(np.zeros((nq, 2)))), N.dptr(N.f64(np.ones(nq))),
+                               N.dptr(N.f64(np.zeros((3, nq, 10)))), nq, N.dptr(N.f64(rule)), N.dptr(N.f64(w)),
+                               N.dptr(N.f64(sh)), 1, C.byref(ctx))
+
+    bad = f.copy()
+    bad[3, 1] = v.shape[0]
+    assert create(bad) == N.HOBI_ERR_VALUE and "references a vertex outside" in N.last_error()
+    assert create(f, nq=17) == N.HOBI_ERR_VALUE and "1..16" in N.last_error()
+    assert create(f, kappa=1e12) == N.HOBI_ERR_VALUE and "supported range" in N.last_error()
+    a = _problem(g)
+    b = _problem(golden("star_l3"))
+    members = (C.c_void_p * 2)(a.handle, b.handle)
+    grp = C.c_void_p()
+    assert lib.hobi_group_create(members, 2, C.byref(grp)) == N.HOBI_ERR_VALUE
+    assert "same problem" in N.last_error()
+    handles = (C.c_ubyte * 64)()
+    assert lib.hobi_comm_p2p_open(a.handle, handles, 1, 0) == N.HOBI_ERR_STATE
