@@ -222,6 +222,11 @@ def test_born_sphere_frozen_energy():
                       SolverConfig(workers=1))
     assert solvation_energy(prob, sol) == pytest.approx(-81.98131581725495, rel=1e-9)
     assert 4 <= sol.iterations <= 9
+    from paper_1301_5914_b200 import surface_potential_error
+    from paper_1301_5914_b200.kirkwood import SphereProblem, kirkwood_centered
+
+    _, exact_phi, _ = kirkwood_centered(SphereProblem(2.0, water, ChargeSystem([[0.0, 0.0, 0.0]], [1.0])))
+    assert surface_potential_error(sol.phi, exact_phi(prob.colloc_pos)) == pytest.approx(7.105e-5, rel=0.05)
     prob, sol = solve(icosahedral_sphere(2, 2.0), water, ChargeSystem([[0.0, 0.0, 0.0]], [1.0]),
                       SolverConfig(scheme="lobi", workers=1))
     assert solvation_energy(prob, sol) == pytest.approx(-86.3199784371863, rel=1e-9)
