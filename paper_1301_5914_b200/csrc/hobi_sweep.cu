@@ -17,6 +17,14 @@
 // (cp.async.bulk + mbarrier).  Source groups depend only on the problem, never
 // on the row split or the tiling, so every row's sum is bitwise identical for
 // any number of GPUs (solver.py:12-17).
+//
+// Instantiations: MODE (screened / kappa = 0), FULL (K3/K4 block too, or the
+// K1/K2-only energy sweep), SELF (LOBI self-pair mask, applied only on source
+// tiles that overlap the item's rows), R targets per thread, MINB CTAs per SM,
+// UNROLL of the source loop, STEP (step-major pair arithmetic).  launch_sweep
+// picks a 768-row tile, falls back to 512-row tiles for ranges with a long
+// remainder and to 128-row tiles for small ranges, and runs the rows past the
+// last whole tile as a second 128-row-tile launch on the side stream.
 #include <algorithm>
 #include <cmath>
 #include <mutex>
