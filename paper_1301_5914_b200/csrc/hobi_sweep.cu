@@ -555,6 +555,17 @@ static const SweepVariant kLaplaceVariants[] = {
     {sweep_kernel<kLaplace, true, false, 4, 3, 2>, 4, "laplace_R4_minb3_unroll2"},
     {sweep_kernel<kLaplace, true, false, 1, 8, 2>, 1, "laplace_R1_minb8_unroll2"},
 };
+// energy sweeps (K1/K2 only, charges as targets), screened and kappa = 0
+static const SweepVariant kEnergyVariants[] = {
+    {sweep_kernel<kScreened, false, false, 6, 2, 2>, 6, "energy_R6_minb2_unroll2"},
+    {sweep_kernel<kScreened, false, false, 4, 3, 2>, 4, "energy_R4_minb3_unroll2"},
+    {sweep_kernel<kScreened, false, false, 1, 8, 2>, 1, "energy_R1_minb8_unroll2"},
+};
+static const SweepVariant kEnergyLaplaceVariants[] = {
+    {sweep_kernel<kLaplace, false, false, 6, 2, 2>, 6, "energy_laplace_R6_minb2_unroll2"},
+    {sweep_kernel<kLaplace, false, false, 4, 3, 2>, 4, "energy_laplace_R4_minb3_unroll2"},
+    {sweep_kernel<kLaplace, false, false, 1, 8, 2>, 1, "energy_laplace_R1_minb8_unroll2"},
+};
 static const SweepVariant kLaplaceSelfVariants[] = {
     {sweep_kernel<kLaplace, true, true, 6, 2, 2>, 6, "laplace_self_R6_minb2_unroll2"},
     {sweep_kernel<kLaplace, true, true, 4, 3, 2>, 4, "laplace_self_R4_minb3_unroll2"},
@@ -609,13 +620,16 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
   } seg[2];
   int nseg = 1;
   seg[0] = {nullptr, kSweepR, t0, t1};
-  if (full) {
+  {
     {
-      // the tuning table for screened HOBI; LOBI (self mask) and kappa = 0 run
-      // the same tile choice on their own wide / narrow / small instantiations
-      const bool tuned = c->phys.mode == kScreened && !self;
+      // the tuning table for screened HOBI; LOBI (self mask), kappa = 0 and
+      // the energy sweep run the same tile choice on their own wide / narrow /
+      // small instantiations
+      const bool scr = c->phys.mode == kScreened;
+      const bool tuned = scr && full && !self;
       const SweepVariant* tab = tuned ? kVariants
-                                : c->phys.mode == kScreened ? kSelfVariants
+                                : !full ? (scr ? kEnergyVariants : kEnergyLaplaceVariants)
+                                : scr ? kSelfVariants
                                 : self ? kLaplaceSelfVariants : kLaplaceVariants;
       const int wide = tuned ? kWideVariant : 0, narrow = tuned ? kNarrowVariant : 1,
                 small = tuned ? kSmallVariant : 2;
@@ -644,9 +658,6 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
         nseg = 2;
       }
     }
-  } else {  // energy: K1/K2 only, charges as targets
-    seg[0].fn = c->phys.mode == kScreened ? sweep_kernel<kScreened, false, false, kSweepR, 1, 2>
-                                          : sweep_kernel<kLaplace, false, false, kSweepR, 1, 2>;
   }
   if (!c->sms) HOBI_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device));
   const int sms = c->sms;
