@@ -650,3 +650,36 @@ def test_c_abi_argument_errors():
     assert "same problem" in N.last_error()
     handles = (C.c_ubyte * 64)()
     assert lib.hobi_comm_p2p_open(a.handle, handles, 1, 0) == N.HOBI_ERR_STATE
+
+
+def test_no_device_memory_leak_across_lifecycles():
+    """Create / use / close contexts, emulated splits, groups and workspaces
+    many times: device memory returns to where it started."""
+    import torch
+
+    from paper_1301_5914_b200.solver import GpuOperator
+
+    g = golden("star_l3")
+
+    def cycle():
+        prob = _problem(g)
+        u = np.random.default_rng(1).standard_normal(prob.n_unknowns)
+        matvec_hobi(prob, u)
+        cfg = SolverConfig(workers=1, restart=int(g["restart"]))
+        with make_operator(prob, cfg) as op:
+            sol = gmres_solve(op, assemble_rhs(prob), cfg)
+        solvation_energy(prob, sol)
+        with GpuOperator(prob, 3) as op:  # emulated split
+            op(u)
+        with GpuOperator(prob, 2, devices=[prob.device] * 2) as op:  # group with a replica
+            gmres_solve(op, assemble_rhs(prob), cfg)
+        prob.close()
+
+    cycle()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(15):
+        cycle()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 16 << 20, (free0 - free1) / 2**20  # < 16 MiB drift (allocator granularity)
