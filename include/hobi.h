@@ -35,6 +35,8 @@ enum hobi_status {
   HOBI_ERR_STATE = 7           /* misuse of the API (wrong order of calls, bad handle)       */
 };
 
+/* A context owns its streams and workspaces: use one from one thread at a time;
+ * different contexts may be driven from different threads concurrently. */
 typedef struct hobi_ctx hobi_ctx;
 
 /* Message of the last failing call on this thread ("" if none). */

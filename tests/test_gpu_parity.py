@@ -683,3 +683,30 @@ def test_no_device_memory_leak_across_lifecycles():
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 16 << 20, (free0 - free1) / 2**20  # < 16 MiB drift (allocator granularity)
+
+
+def test_concurrent_contexts_from_threads():
+    """Different contexts driven from different threads at once (each has its
+    own streams and workspaces) give the sequential results bit for bit."""
+    import threading
+
+    names = ["star_l2", "star_l3", "c1", "uv_sphere"]
+    probs = {n: _problem(golden(n)) for n in names}
+    us = {n: np.random.default_rng(7).standard_normal(p.n_unknowns) for n, p in probs.items()}
+    ref = {n: matvec_hobi(probs[n], us[n]) for n in names}
+    errors = []
+
+    def run(n):
+        try:
+            for _ in range(5):
+                if not np.array_equal(matvec_hobi(probs[n], us[n]), ref[n]):
+                    errors.append(n)
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=run, args=(n,)) for n in names]  # one thread per context
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
