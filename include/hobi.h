@@ -190,8 +190,10 @@ int hobi_comm_p2p_open(hobi_ctx* ctx, const unsigned char* handles, int nranks, 
  * `members` are contexts of the same problem, usually one per device
  * (member 0 leads: inputs, outputs and GMRES live there); member i owns rows
  * partition_targets(n_colloc, size)[i].  Each application copies the iterate
- * peer-to-peer to the members, runs every member's rows on its own device and
- * copies them back; devices are ordered by events only, so members may also
+ * peer-to-peer to the members and runs every member's rows on its own device;
+ * each member's epilogue kernel stores its rows straight into the leader's
+ * output over peer memory (a staged copy where peer access is unavailable).
+ * Devices are ordered by events only, so members may also
  * share a device.  Results are bitwise those of one context.  Members must
  * outlive every group call and must not be in a communicator or emulated
  * split; hobi_group_destroy touches only the group's own buffers.

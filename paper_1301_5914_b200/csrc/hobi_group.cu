@@ -5,14 +5,18 @@
 // (replicated, as in the one-process-per-GPU mode).  Member i owns rows
 // partition_targets(n, size)[i].  One application: the leader's input is
 // copied peer-to-peer to every member (NVLink on an NVSwitch box), each member
-// runs the sweep + epilogue of its rows on its own streams, copies its [2][m]
-// slot back into the leader's rank-major receive buffer, and the leader waits
-// on every member's event and permutes.  Only event waits order the devices --
+// runs the sweep + epilogue of its rows on its own streams, and the epilogue
+// kernel stores its finished rows straight into the leader's output vector
+// over peer memory -- the gather is fused into the compute kernel, in final
+// layout, with no staging buffer and no permutation; the leader waits on
+// every member's event.  Without peer access a member stages its [2][m] slot
+// and copies it over instead.  Only event waits order the devices --
 // no kernel waits on another -- so members may share a device (that is how
 // the path is tested on one GPU).  Rows are bitwise identical for any split,
 // so a group solve equals the one-GPU solve bit for bit.  GMRES runs on the
 // leader through the same device-resident solver.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "hobi_internal.cuh"
@@ -22,7 +26,8 @@ namespace {
 
 struct Member {
   hobi_ctx* c = nullptr;
-  int device = 0;  // kept so the group can be released after its members
+  int device = 0;       // kept so the group can be released after its members
+  bool direct = false;  // epilogue stores straight into the leader's output (peer access)
   int64_t lo = 0, hi = 0;
   DevBuf<double> u, slot;  // input copy and [2][m] output slot on the member's device
   cudaEvent_t done = nullptr;
@@ -61,17 +66,38 @@ struct GroupOperator : DeviceOperator {
         HOBI_CUDA(cudaMemcpyPeerAsync(mb.u.p, c->device, in, lead->device, bytes, c->stream));
         u = mb.u.p;
       }
-      int rc = matvec_rows_device(c, u, mb.lo, mb.hi, mb.slot.p, mb.slot.p + g->slot_m);
-      if (rc) return rc;
-      HOBI_CUDA(cudaMemcpyPeerAsync(g->recv.p + i * 2 * g->slot_m, lead->device, mb.slot.p, c->device,
-                                    2 * g->slot_m * sizeof(double), c->stream));
+      int rc;
+      if (mb.direct) {
+        // fused gather: the epilogue kernel's row stores land in the leader's
+        // output vector (NVLink peer stores), final layout, nothing to permute
+        rc = matvec_rows_device(c, u, mb.lo, mb.hi, out + mb.lo, out + g->nt + mb.lo);
+        if (rc) return rc;
+      } else {  // no peer access: stage the rows and copy them over
+        rc = matvec_rows_device(c, u, mb.lo, mb.hi, mb.slot.p, mb.slot.p + g->slot_m);
+        if (rc) return rc;
+        HOBI_CUDA(cudaMemcpyPeerAsync(g->recv.p + i * 2 * g->slot_m, lead->device, mb.slot.p, c->device,
+                                      2 * g->slot_m * sizeof(double), c->stream));
+      }
       HOBI_CUDA(cudaEventRecord(mb.done, c->stream));
     }
     HOBI_CUDA(cudaSetDevice(lead->device));
-    for (Member& mb : g->m) HOBI_CUDA(cudaStreamWaitEvent(lead->stream, mb.done, 0));
-    int rc = permute_rows(lead->stream, g->recv.p, g->slot_m, g->nt, (int)g->m.size(), out);
-    lead->launches++;
-    return rc;
+    bool staged = false;
+    for (Member& mb : g->m) {
+      HOBI_CUDA(cudaStreamWaitEvent(lead->stream, mb.done, 0));
+      staged |= !mb.direct;
+    }
+    if (!staged) return 0;
+    // staged members: their slots arrived in the leader's receive buffer
+    for (size_t i = 0; i < g->m.size(); ++i) {
+      const Member& mb = g->m[i];
+      if (mb.direct || mb.hi <= mb.lo) continue;
+      const double* slot = g->recv.p + i * 2 * g->slot_m;
+      HOBI_CUDA(cudaMemcpyAsync(out + mb.lo, slot, (mb.hi - mb.lo) * sizeof(double),
+                                cudaMemcpyDeviceToDevice, lead->stream));
+      HOBI_CUDA(cudaMemcpyAsync(out + g->nt + mb.lo, slot + g->slot_m, (mb.hi - mb.lo) * sizeof(double),
+                                cudaMemcpyDeviceToDevice, lead->stream));
+    }
+    return 0;
   }
 };
 
@@ -117,11 +143,16 @@ int hobi_group_create(hobi_ctx* const* members, int size, hobi_group** out) {
   cudaError_t e = cudaEventCreateWithFlags(&g->in_ready, cudaEventDisableTiming);
   if (e != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
   // peer access between distinct devices (NVLink); same-device members need none
+  g->m[0].direct = true;
   for (int i = 1; i < size; ++i) {
     const int d = members[i]->device;
-    if (d == lead->device) continue;
+    if (d == lead->device) {
+      g->m[i].direct = !getenv("HOBI_GROUP_STAGED");  // test hook: force the staged path
+      continue;
+    }
     int ok = 0;
-    cudaDeviceCanAccessPeer(&ok, lead->device, d);
+    cudaDeviceCanAccessPeer(&ok, d, lead->device);
+    g->m[i].direct = ok && !getenv("HOBI_GROUP_STAGED");
     if (ok) {
       cudaSetDevice(lead->device);
       e = cudaDeviceEnablePeerAccess(d, 0);

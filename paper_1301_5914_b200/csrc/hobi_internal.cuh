@@ -248,8 +248,6 @@ int comm_allgather(hobi_ctx* c);
 int comm_allgather_bytes(hobi_ctx* c, const void* send, void* recv, size_t bytes);
 // gathered [rank][2][m] slots -> out[0:nt] ++ out[nt:2nt] (hobi_sweep.cu)
 int gather_permute(hobi_ctx* c, double* out_dev);
-int permute_rows(cudaStream_t stream, const double* recv, int64_t m, int64_t nt, int nranks,
-                 double* out_dev);
 int p2p_check(hobi_ctx* c);
 
 }  // namespace hobi

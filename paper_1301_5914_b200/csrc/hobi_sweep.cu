@@ -867,14 +867,6 @@ int p2p_check(hobi_ctx* c) {
   return 0;
 }
 
-// Rank-major [r][2][m] rows -> out (phi rows then dphi rows), on `stream`.
-int permute_rows(cudaStream_t stream, const double* recv, int64_t m, int64_t nt, int nranks,
-                 double* out_dev) {
-  permute_kernel<<<nblk(nt, 256), 256, 0, stream>>>(recv, m, nt, nranks, out_dev);
-  HOBI_CUDA(cudaGetLastError());
-  return 0;
-}
-
 int gather_permute(hobi_ctx* c, double* out_dev) {
   permute_kernel<<<nblk(c->nt, 256), 256, 0, c->stream>>>(c->gather_recv.p, c->gather_m, c->nt,
                                                            c->comm.nranks, out_dev);

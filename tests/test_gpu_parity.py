@@ -560,14 +560,17 @@ def test_lobi_self_mask_tiles_bitwise_across_splits():
     p4.close()
 
 
-@pytest.mark.parametrize("scheme", ["hobi", "lobi"])
-def test_single_process_group_operator_bitwise(scheme):
+@pytest.mark.parametrize("scheme,staged", [("hobi", False), ("lobi", False), ("hobi", True)])
+def test_single_process_group_operator_bitwise(scheme, staged, monkeypatch):
     """The single-process multi-GPU group (workers -> GPUs without torchrun):
-    replicas on the problem's device stand in for peers (copies between
-    members are ordered by events only, so sharing a device is legal).  The
-    group matvec and the group GMRES solve are bitwise those of one context."""
+    replicas on the problem's device stand in for peers (members are ordered
+    by events only, so sharing a device is legal).  Fused path: every member's
+    epilogue stores its rows into the leader's output; staged path: slots are
+    copied over.  The group matvec and GMRES solve are bitwise one context's."""
     from paper_1301_5914_b200.solver import GpuOperator
 
+    if staged:  # members without peer access stage their rows and copy them over
+        monkeypatch.setenv("HOBI_GROUP_STAGED", "1")
     g = golden("star_l3")
     prob = _problem(g, scheme=scheme)
     cfg = SolverConfig(workers=1, restart=int(g["restart"]), scheme=scheme)
