@@ -40,7 +40,7 @@ struct hobi_group {
   std::vector<hobi::Member> m;
   int64_t nt = 0, slot_m = 0;
   hobi::DevBuf<double> recv;  // leader: [size][2][slot_m]
-  cudaEvent_t in_ready = nullptr, gathered = nullptr;
+  cudaEvent_t in_ready = nullptr;
   hobi::GmresWorkspace gmres_ws;
 };
 
