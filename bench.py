@@ -60,8 +60,9 @@ def _args():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0, help="rows per CPU sample (0 = auto)")
-    ap.add_argument("--gather", choices=("nccl", "p2p"), default=os.environ.get("HOBI_GATHER", "nccl"),
-                    help="N>1 row gather: ncclAllGather, or the fused epilogue + NVLink peer stores")
+    ap.add_argument("--gather", choices=("auto", "nccl", "p2p"), default=os.environ.get("HOBI_GATHER", "auto"),
+                    help="N>1 row gather: fused epilogue + NVLink peer stores when a start-up check "
+                         "matches the NCCL gather (auto), always (p2p), or ncclAllGather (nccl)")
     return ap.parse_args()
 
 
@@ -385,8 +386,11 @@ def run_ours(a):
                 "frac_of_64": ops / 64.0, "sms": sms.value, "sm_mhz": clk["sm_mhz"]}
     if rank == 0:
         conf = _workload(cfg, nv, nf, nq)
-        conf["parallelism"] = (f"row split x{world} + " + ("NCCL allgather" if a.gather == "nccl" else
-                               "fused epilogue/NVLink peer-store gather")) if world > 1 else "single GPU"
+        p2p_on = C.c_int(0)
+        N.check(lib.hobi_comm_info(h, None, None, C.byref(p2p_on)))
+        conf["parallelism"] = (f"row split x{world} + " + ("fused epilogue/NVLink peer-store gather"
+                                                            if p2p_on.value else "NCCL allgather")
+                               + f" (--gather {a.gather})") if world > 1 else "single GPU"
         line = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,

@@ -183,6 +183,11 @@ int hobi_comm_init(hobi_ctx* ctx, const unsigned char id[128], int nranks, int r
  */
 int hobi_comm_p2p_handle(hobi_ctx* ctx, unsigned char handle[64]);
 int hobi_comm_p2p_open(hobi_ctx* ctx, const unsigned char* handles, int nranks, int rank);
+/* Fall back from the peer-store gather to the communicator's ncclAllGather
+ * (permanently, e.g. when a start-up check of the P2P path fails). */
+int hobi_comm_p2p_disable(hobi_ctx* ctx);
+/* Row-split state: ranks, this rank, and whether the P2P gather is active. */
+int hobi_comm_info(hobi_ctx* ctx, int* nranks, int* rank, int* p2p);
 
 /*
  * Single-process multi-GPU group (SolverConfig.workers -> GPUs without

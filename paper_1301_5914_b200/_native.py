@@ -54,6 +54,8 @@ SIGNATURES = {
     "hobi_gmres_host_operator": (C.c_int, [C.c_int, C.c_int64, APPLY_FN, C.c_void_p, _dp, C.c_double,
                                            C.c_int, C.c_int, _dp, C.POINTER(C.c_int), _dp, _dp,
                                            C.POINTER(C.c_int)]),
+    "hobi_comm_p2p_disable": (C.c_int, [_ctxp]),
+    "hobi_comm_info": (C.c_int, [_ctxp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "hobi_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p)]),
     "hobi_group_destroy": (C.c_int, [C.c_void_p]),
     "hobi_group_matvec": (C.c_int, [C.c_void_p, _dp, _dp]),

@@ -772,6 +772,22 @@ int hobi_comm_p2p_open(hobi_ctx* c, const unsigned char* handles, int nranks, in
   return 0;
 }
 
+int hobi_comm_p2p_disable(hobi_ctx* c) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  c->comm.p2p = false;  // the NCCL gather (set up by hobi_comm_init) takes over
+  return 0;
+}
+
+int hobi_comm_info(hobi_ctx* c, int* nranks, int* rank, int* p2p) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (nranks) *nranks = c->comm.nranks;
+  if (rank) *rank = c->comm.rank;
+  if (p2p) *p2p = c->comm.p2p ? 1 : 0;
+  return 0;
+}
+
 int hobi_emulate_ranks(hobi_ctx* c, int nranks) {
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   if (nranks < 1) return fail(HOBI_ERR_VALUE, "nranks must be >= 1");

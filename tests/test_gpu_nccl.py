@@ -98,3 +98,40 @@ def test_p2p_missing_peer_times_out_instead_of_hanging(monkeypatch):
         matvec_hobi(prob, g["u"])
     assert time.monotonic() - t0 < 30.0
     prob.close()
+
+
+@pytest.mark.parametrize("break_p2p", [False, True])
+def test_auto_gather_startup_check(monkeypatch, tmp_path, break_p2p):
+    """HOBI_GATHER=auto: the P2P gather is switched on only after it matches
+    the NCCL gather bit for bit; a P2P path whose arrivals never complete
+    (test hook + short watchdog) is detected and every rank stays on NCCL."""
+    torch = pytest.importorskip("torch")
+    import torch.distributed as dist
+
+    from paper_1301_5914_b200 import ChargeSystem, FlatMesh, PhysicalParams, SolverConfig, discretize, matvec_hobi
+    from paper_1301_5914_b200 import _native as N
+    from paper_1301_5914_b200.distributed import init_p2p_gather_checked
+
+    g = golden("star_l3")
+    mesh = FlatMesh(g["vertices"], g["normals"], g["faces"])
+    params, charges = PhysicalParams(*g["params"]), ChargeSystem(g["qpos"], g["q"])
+    ref = matvec_hobi(discretize(mesh, params, charges, SolverConfig(workers=1)), g["u"])
+    prob = discretize(mesh, params, charges, SolverConfig(workers=1))
+    lib = N.load()
+    uid = (C.c_ubyte * 128)()
+    N.check(lib.hobi_comm_unique_id(uid))
+    monkeypatch.setenv("HOBI_FORCE_NCCL", "1")
+    N.check(lib.hobi_comm_init(prob.handle, uid, 1, 0))
+    if break_p2p:
+        monkeypatch.setenv("HOBI_P2P_TIMEOUT_MS", "300")
+        monkeypatch.setenv("HOBI_P2P_TEST_MISSING_ARRIVALS", "1")
+    dist.init_process_group("gloo", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+    try:
+        active = init_p2p_gather_checked(prob.handle, 0, 1)
+    finally:
+        dist.destroy_process_group()
+    info = C.c_int(-1)
+    N.check(lib.hobi_comm_info(prob.handle, None, None, C.byref(info)))
+    assert active == (not break_p2p) and info.value == int(active)
+    assert np.array_equal(matvec_hobi(prob, g["u"]), ref)  # P2P or NCCL, same bits
+    prob.close()
