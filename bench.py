@@ -6,7 +6,8 @@
 
 A step is one application of the HOBI operator (SURVEY.md 8(a) rows a11-a14:
 source weights, all-pairs regular sweep, Duffy swap, diagonal, and for N > 1
-the NCCL allgather of the row split) to a seeded u on BASELINE.json config 4
+the gather of the row split: epilogue peer stores over NVLink once a start-up
+check matches ncclAllGather bit for bit, else ncclAllGather) to a seeded u on BASELINE.json config 4
 (star surface, icosphere level 6, 81,920 triangles, row-sharded at 1/2/4/8
 GPUs).  The unit of work is one regular pair (target vertex, source regular
 quadrature point): N_v * 4 N_f = 1.342e10 pairs per step.
