@@ -66,6 +66,18 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
                 hobi_ctx** out);
 
 /*
+ * hobi_create with the reference's default rules built in: the 4-point
+ * conical Gauss-Radau regular rule and the duffy_points x duffy_points Duffy
+ * rule (duffy_points in {4, 6, 8}; SolverConfig's default is 4), with their
+ * cubic shape tables (quadrature.py:68-116, geometry.py:197-205) -- the same
+ * bits the Python host computes, so a C/C++ integrator gets the same caches
+ * without any quadrature code of its own.
+ */
+int hobi_create_default(int device, const double* vertices, const double* normals, int64_t nv,
+                        const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
+                        int duffy_points, hobi_ctx** out);
+
+/*
  * Build a HOBI context from caches computed elsewhere -- e.g. the fields of
  * the reference's own DiscretizedProblem (solver.py:122-140: reg_pos/nrm/w,
  * reg_bary, duf_pos/nrm/w, duf_bary, pair_vertex/face/gverts/starts, in the

@@ -29,7 +29,7 @@ UNITS = {
     "hobi_geometry.cu": ["-fmad=false"],
     "hobi_literal.cu": ["-fmad=false"],
 }
-HEADERS = ["hobi_internal.cuh", "hobi_fastmath.cuh"]
+HEADERS = ["hobi_internal.cuh", "hobi_fastmath.cuh", "hobi_default_rules.inc"]
 
 
 def _nvcc():

@@ -352,6 +352,22 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
   return 0;
 }
 
+namespace {
+#include "hobi_default_rules.inc"
+}  // namespace
+
+int hobi_create_default(int device, const double* vertices, const double* normals, int64_t nv,
+                        const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
+                        int duffy_points, hobi_ctx** out) {
+  *out = nullptr;
+  for (const DefDuffy& d : kDefDuffy)
+    if (d.n == duffy_points)
+      return hobi_create(device, vertices, normals, nv, faces, nf, eps1, eps2, kappa, kDefRegPts, kDefRegWts,
+                         kDefRegShape, 4, d.pts, d.wts, d.shape, d.n * d.n, out);
+  return fail(HOBI_ERR_VALUE, "hobi_create_default: duffy_points must be 4, 6 or 8, got " +
+                                  std::to_string(duffy_points));
+}
+
 int hobi_create_from_caches(int device, const double* vertices, const double* normals, int64_t nv,
                             const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
                             const double* reg_pos, const double* reg_nrm, const double* reg_w,

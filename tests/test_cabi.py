@@ -3,6 +3,7 @@ declares (no compute calls without a GPU); the product refuses to run
 without a device instead of falling back to the CPU."""
 
 import os
+import sys
 import re
 
 import numpy as np
@@ -129,4 +130,29 @@ def test_header_is_plain_c():
         open(c_file, "w").write(src)
         out = subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-pedantic", "-fsyntax-only",
                               "-I", os.path.join(ROOT, "include"), c_file], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+
+
+def test_default_rule_tables_are_generated_from_the_python_rules():
+    """csrc/hobi_default_rules.inc (hobi_create_default's tables) is exactly
+    what tools/gen_default_rules.py produces from quadrature.py."""
+    import subprocess
+
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_default_rules.py"), "--check"],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, "regenerate with python tools/gen_default_rules.py"
+
+
+def test_c_example_compiles():
+    import shutil
+    import subprocess
+    import tempfile
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    with tempfile.TemporaryDirectory() as tmp:
+        out = subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-pedantic", "-I", os.path.join(ROOT, "include"),
+                              os.path.join(ROOT, "examples", "c_solve.c"), "-L", os.path.dirname(N.LIB_PATH),
+                              "-lhobi", "-o", os.path.join(tmp, "c_solve")], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr

@@ -713,3 +713,37 @@ def test_concurrent_contexts_from_threads():
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+def test_c_host_example_matches_python_path(tmp_path):
+    """examples/c_solve.c -- a plain C program on the C ABI with the built-in
+    default rules (hobi_create_default + hobi_solve) -- reproduces the Python
+    path's solve bit for bit (same caches, same GMRES, same energy)."""
+    import os
+    import shutil
+    import subprocess
+
+    from paper_1301_5914_b200 import _native as N
+    from paper_1301_5914_b200 import icosahedral_sphere, solve
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "c_solve")
+    libdir = os.path.dirname(N.LIB_PATH)
+    subprocess.run([cc, "-std=c99", "-I", os.path.join(root, "include"), os.path.join(root, "examples", "c_solve.c"),
+                    "-L", libdir, "-lhobi", f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    mesh = icosahedral_sphere(2, 2.0)
+    params = PhysicalParams(1.0, 80.0, 0.1257)
+    charges = ChargeSystem([[0.1, -0.2, 0.3], [-0.4, 0.0, 0.2]], [1.0, -0.5])
+    blob = (np.array([mesh.n_vertices, mesh.n_faces, 2], dtype=np.int64).tobytes()
+            + np.array([params.eps1, params.eps2, params.kappa]).tobytes()
+            + N.f64(mesh.vertices).tobytes() + N.f64(mesh.normals).tobytes()
+            + N.i64(mesh.faces).tobytes() + N.f64(charges.positions).tobytes() + N.f64(charges.charges).tobytes())
+    (tmp_path / "problem.bin").write_bytes(blob)
+    out = subprocess.run([exe, str(tmp_path / "problem.bin")], capture_output=True, text=True, check=True)
+    its, mvs, res, e_hex = out.stdout.split()
+    prob, sol = solve(mesh, params, charges, SolverConfig(workers=1))
+    assert int(its) == sol.iterations and int(mvs) == sol.matvecs
+    assert float.fromhex(e_hex) == solvation_energy(prob, sol)
