@@ -244,6 +244,19 @@ int hobi_sweep_variant(hobi_ctx* ctx, int variant, int* count, char* name, int n
  * padded source count -- for the algorithmic-bytes accounting of bench.py. */
 int hobi_sweep_layout(hobi_ctx* ctx, int* n_groups, int64_t* n_sources_padded);
 
+/*
+ * MSMS ingest fast path (host only, no device needed): parse_msms's record
+ * rules (mesh.py; reference mesh.py:141-185) on the .vert/.face texts, one pass.
+ * Fills vdata (up to vert_cap rows of x y z nx ny nz as written) and faces
+ * (up to face_cap rows, 0-based) and reports the record counts; the number of
+ * lines of each text is a sufficient capacity.  Returns HOBI_ERR_VALUE
+ * ("irregular") whenever the text has anything the Python parser might read
+ * differently or would reject -- the caller then runs the Python parser,
+ * which gives the reference's exact result or error.
+ */
+int hobi_msms_parse(const char* vert, int64_t vert_len, const char* face, int64_t face_len, double* vdata,
+                    int64_t vert_cap, int64_t* faces, int64_t face_cap, int64_t* n_vert, int64_t* n_face);
+
 /* Regular pairs per full matvec (N_v x N_f x nq for hobi), for throughput. */
 int hobi_pairs_per_matvec(hobi_ctx* ctx, double* pairs);
 

@@ -58,6 +58,8 @@ SIGNATURES = {
     "hobi_comm_info": (C.c_int, [_ctxp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "hobi_create_default": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _i64p, C.c_int64, C.c_double, C.c_double,
                                       C.c_double, C.c_int, C.POINTER(C.c_void_p)]),
+    "hobi_msms_parse": (C.c_int, [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, _dp, C.c_int64, _i64p, C.c_int64,
+                                  _i64p, _i64p]),
     "hobi_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p)]),
     "hobi_group_destroy": (C.c_int, [C.c_void_p]),
     "hobi_group_matvec": (C.c_int, [C.c_void_p, _dp, _dp]),

@@ -26,6 +26,7 @@ UNITS = {
     "hobi_sweep.cu": [],
     "hobi_gmres.cu": [],
     "hobi_group.cu": [],
+    "hobi_msms.cu": [],
     "hobi_geometry.cu": ["-fmad=false"],
     "hobi_literal.cu": ["-fmad=false"],
 }
