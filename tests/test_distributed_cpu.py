@@ -86,3 +86,24 @@ def test_layout_round_trip(n, world):
     for r in range(world):
         lo, hi = D.row_range(n, world, r)
         assert np.all(owners[lo:hi] == r)
+
+
+def _agree_worker(rank, world, port, result_dir):
+    """_all_true, the step agreement of the auto gather check, and the P2P
+    handle exchange's failure handling without a device."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = [D._all_true(True), D._all_true(rank != 1), D._all_true(False)]
+    with open(os.path.join(result_dir, f"agree{rank}"), "w") as f:
+        f.write(" ".join(str(int(r)) for r in res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_step_agreement_gloo(tmp_path):
+    """Every rank reaches the same decision even when one rank's local check
+    fails -- so no rank proceeds into a P2P collective the others skip."""
+    world = 3
+    mp.spawn(_agree_worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert open(tmp_path / f"agree{r}").read() == "1 0 0"
