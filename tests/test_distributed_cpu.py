@@ -89,8 +89,7 @@ def test_layout_round_trip(n, world):
 
 
 def _agree_worker(rank, world, port, result_dir):
-    """_all_true, the step agreement of the auto gather check, and the P2P
-    handle exchange's failure handling without a device."""
+    """_all_true: the step agreement of the auto gather check."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     res = [D._all_true(True), D._all_true(rank != 1), D._all_true(False)]
