@@ -15,9 +15,9 @@ quadrature point): N_v * 4 N_f = 1.342e10 pairs per step.
 `value`   : pairs/s, u resident in HBM, device time (CUDA events on the
             library's stream), L2 flushed between steps, max over ranks.
 `e2e`     : the same through the call a user makes -- the operator protocol
-            op(u) on host numpy arrays (H2D of u, matvec, D2H of A u inside
-            every call), wall clock, max over ranks; `e2e.device_events` is the
-            pinned host-buffer C-ABI step timed with CUDA events.
+            op(u, out=...) on pinned host arrays (H2D of u, matvec, D2H of A u
+            inside every call), wall clock, max over ranks; `e2e.device_events`
+            is the pinned host-buffer C-ABI step timed with CUDA events.
 `roofline`: the all-pairs sweep kernel, 96 canonical FP64 flops per pair
              over its event-timed duration, against the FP64
             DFMA peak measured in the same run (MEASURED_PEAKS.json has none).
@@ -304,16 +304,19 @@ def run_ours(a):
     except Exception:  # noqa: BLE001
         flush = None
     api_wall = []
+    u_api, out_api = u, None
+    if pinned:  # the step's input and result live in pinned host memory (views of hu / ho)
+        u_api, out_api = hu.numpy(), ho.numpy()
     with make_operator(prob, scfg) as op_api:
         for _ in range(a.warmup):
-            op_api(u)
+            op_api(u_api, out=out_api)
         barrier()
         for _ in range(a.steps):
             if flush is not None:
                 flush.fill_(1.0)
                 torch.cuda.synchronize()
             t0 = time.perf_counter()
-            op_api(u)
+            op_api(u_api, out=out_api)
             api_wall.append(time.perf_counter() - t0)
     api_ms = max_over_ranks(1e3 * float(sum(api_wall)))
     api = a.steps * pairs_step / (api_ms * 1e-3)
@@ -399,10 +402,12 @@ def run_ours(a):
             "config": conf,
             "e2e": {"value": api, "unit": "pairs/s", "h2d_bytes_per_step": 16 * nv * world,
                     "d2h_bytes_per_step": 16 * nv * world, "ms_per_step": api_ms / a.steps,
-                    "how": "wall clock of the public operator call op(u) on host numpy arrays "
-                           "(make_operator, solver.py:447-459), H2D + matvec + D2H inside each call, "
-                           "max over ranks; L2 flushed between calls" + ("" if flush is not None
-                                                                        else " (flush unavailable)"),
+                    "pinned": pinned,
+                    "how": "wall clock of the public operator call op(u, out=...) on host arrays "
+                           "(make_operator, solver.py:447-459), "
+                           + ("pinned " if pinned else "pageable ")
+                           + "H2D + matvec + D2H inside each call, max over ranks; L2 flushed between "
+                           "calls" + ("" if flush is not None else " (flush unavailable)"),
                     "device_events": {"value": e2e, "ms_per_step": e2e_ms / a.steps, "pinned": pinned,
                                       "how": "hobi_bench mode 1: pinned H2D + matvec + D2H between "
                                              "CUDA events on the library stream"}},

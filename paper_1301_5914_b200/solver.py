@@ -360,9 +360,18 @@ def _as_vector(problem, u):
     return u
 
 
-def _full_matvec(problem: DiscretizedProblem, u) -> np.ndarray:
+def _out_vector(u: np.ndarray, out):
+    if out is None:
+        return np.empty_like(u)
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == u.shape
+            and out.flags.c_contiguous and out.flags.writeable):
+        raise ValueError(f"out must be a writable contiguous float64 array of shape {u.shape}")
+    return out
+
+
+def _full_matvec(problem: DiscretizedProblem, u, out=None) -> np.ndarray:
     u = _as_vector(problem, u)
-    out = np.empty_like(u)
+    out = _out_vector(u, out)
     _raise(N.load().hobi_matvec(problem.handle, N.dptr(u), N.dptr(out)))
     return out
 
@@ -464,13 +473,15 @@ class GpuOperator:
         """Native multi-GPU group handle, or None."""
         return self._group
 
-    def __call__(self, u) -> np.ndarray:
+    def __call__(self, u, out=None) -> np.ndarray:
+        """A u (solver.py:447-459).  `out` (extension): a float64 array to
+        write into, e.g. pinned host memory for the fastest copies."""
         if self._closed:
             raise ValueError("operator is closed")
         if self._group is None:
-            return _full_matvec(self._problem, u)
+            return _full_matvec(self._problem, u, out)
         u = _as_vector(self._problem, u)
-        out = np.empty_like(u)
+        out = _out_vector(u, out)
         _raise(N.load().hobi_group_matvec(self._group, N.dptr(u), N.dptr(out)))
         return out
 
