@@ -747,3 +747,21 @@ def test_c_host_example_matches_python_path(tmp_path):
     prob, sol = solve(mesh, params, charges, SolverConfig(workers=1))
     assert int(its) == sol.iterations and int(mvs) == sol.matvecs
     assert float.fromhex(e_hex) == solvation_energy(prob, sol)
+
+
+def test_operator_out_buffer():
+    """op(u, out=buf) writes into the caller's array (e.g. pinned memory) and
+    returns it; wrong dtype / shape / a read-only array are rejected."""
+    g = golden("star_l2")
+    prob = _problem(g)
+    with make_operator(prob, SolverConfig(workers=1)) as op:
+        ref = op(g["u"])
+        buf = np.empty_like(ref)
+        assert op(g["u"], out=buf) is buf and np.array_equal(buf, ref)
+        for bad in (np.empty(ref.size, dtype=np.float32), np.empty(ref.size + 2), np.empty((2, ref.size // 2))):
+            with pytest.raises(ValueError, match="out must be"):
+                op(g["u"], out=bad)
+        ro = np.empty_like(ref)
+        ro.setflags(write=False)
+        with pytest.raises(ValueError, match="out must be"):
+            op(g["u"], out=ro)
