@@ -11,7 +11,7 @@ import sys
 import numpy as np
 sys.path.insert(0, '.'); sys.path.insert(0, 'oracle')
 import hobi_oracle as O
-from paper_1301_5914_b200 import (ChargeSystem, PhysicalParams, SolverConfig, SurfaceSolution, discretize,
+from paper_1301_5914_b200 import (PhysicalParams, SolverConfig, SurfaceSolution, discretize,
                                   matvec_hobi, solvation_energy)
 from paper_1301_5914_b200.surfaces import StarShape
 
