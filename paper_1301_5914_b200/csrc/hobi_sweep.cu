@@ -885,7 +885,8 @@ int charge_workspace(hobi_ctx* c, int64_t nc) {
   w.n_groups = (int)gtab.size();
   if (w.q.alloc(nc) || w.qpos.alloc(3 * nc) || w.tq.alloc(6 * ldc) || w.e.alloc(1) ||
       w.groups.alloc(gtab.size()) || w.part.alloc((size_t)w.n_groups * 2 * ldc) || w.v.alloc(nc) ||
-      w.recv.alloc(nc + 64) || w.bad.alloc(1) || w.bad_all.alloc(1024))
+      w.recv.alloc(nc + 64) || w.bad.alloc(1) ||
+      w.bad_all.alloc(std::max<int64_t>(1024, c->comm.nranks)))
     return HOBI_ERR_CUDA;
   HOBI_CUDA(cudaMemcpy(w.groups.p, gtab.data(), gtab.size() * sizeof(int2), cudaMemcpyHostToDevice));
   w.nc = nc;
