@@ -765,3 +765,22 @@ def test_operator_out_buffer():
         ro.setflags(write=False)
         with pytest.raises(ValueError, match="out must be"):
             op(g["u"], out=ro)
+
+
+@pytest.mark.parametrize("restart", [1, 2, 3, 5])
+def test_short_restart_cycles_match_oracle_gmres(restart):
+    """Restart lengths down to 1 (every cycle a true-residual restart,
+    solver.py:509-560): iterations, matvec counts and the solution follow the
+    oracle's GMRES on the oracle's operator."""
+    import hobi_oracle as O
+
+    g = golden("star_l2")
+    prob = _problem(g)
+    o = O.discretize(g["vertices"], g["normals"], g["faces"], *g["params"], g["qpos"], g["q"])
+    b = assemble_rhs(prob)
+    x, its, rel, nmv = O.gmres(lambda v: O.matvec(o, v), O.rhs(o), tol=1e-6, restart=restart, max_it=2000)
+    cfg = SolverConfig(workers=1, restart=restart, max_iterations=2000)
+    with make_operator(prob, cfg) as op:
+        sol = gmres_solve(op, b, cfg)
+    assert sol.iterations == its and sol.matvecs == nmv
+    assert rel_l2(sol.vector, x) <= 1e-9
