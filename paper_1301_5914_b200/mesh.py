@@ -171,9 +171,10 @@ def _split(v, f):
 
 
 def unit_icosphere(level: int):
-    """Unit-sphere vertices and faces of the level-`level` subdivided icosahedron."""
-    if not 0 <= level <= 8:
-        raise ValueError(f"refinement level must be in [0, 8], got {level}")
+    """Unit-sphere vertices and faces of the level-`level` subdivided icosahedron
+    (levels 0-9; the reference-facing icosahedral_sphere keeps its 0-7)."""
+    if not 0 <= level <= 9:
+        raise ValueError(f"refinement level must be in [0, 9], got {level}")
     v, f = _base_icosahedron()
     for _ in range(level):
         v, f = _split(v, f)
