@@ -22,8 +22,8 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   double t = x * y;
   double e = fma(-t, y, 1.0);
   double c = fma(e, 0.375, 0.5);
-  double ye = y * e;
-  return fma(ye, c, y);
+  double ec = e * c;
+  return fma(y, ec, y);  // y read twice: two distinct registers, full DFMA rate
 }
 
 // exp(-x) - 1 for 0 <= x < 1e12, computed as S(1+p) - 1 with S = 2^(k/2048)
@@ -52,21 +52,24 @@ __device__ __forceinline__ double expm1_neg(double x, const double* __restrict__
   return fma(S, p, S - 1.0);
 }
 
-// Screened pair (kappa > 0), scaled coordinates.  Source record:
-//   m' = M m with M = k^3 wp/4pi (the source normal carries the wp weight),
-//   W1 = -k wd/4pi, C = k^2 wd/(4pi er), D = -k^2 (1-1/er) wd/4pi,
-// and two launch constants Ap = er/k, Bp = (er-1)/k (so M (a Ap + Bp) =
-// k^2 wp (a er + er - 1)/4pi).  With dny' = d.m' = M dny, u = dny'/r^2:
-//   K1 wd + K2 wp = (1/r) (W1 em1 + u (a Ap + Bp))
-//   K3 wd + K4 wp = (1/r^3) (dnx (t2 - u b) + a nn')
-// where t2 = a C + D, b = 3a + kr*kre (kernels.py:119-120), nn' = n.m'.
-// acc1 += K1 wd + K2 wp ; acc2 += K3 wd + K4 wp   (solver.py:333-334)
-// 45 FP64 instructions per pair (25 DFMA, 14 DMUL, 6 DADD).
+// Screened pair (kappa > 0), scaled coordinates.  With Ap = er/k and
+// Bp = (er-1)/k the source record holds
+//   m' = M m with M = Ap k^3 wp/4pi (the source normal carries the wp weight),
+//   W1 = -k wd/4pi, C = Ap k^2 wd/(4pi er), D = -Ap k^2 (1-1/er) wd/4pi,
+// and one launch constant Bq = Bp/Ap, so M (a + Bq) = k^2 wp (a er + er - 1)/4pi
+// and the K2 factor needs a DADD instead of a three-register DFMA.  With
+// dny' = d.m' = M dny, u = dny'/r^2:
+//   K1 wd + K2 wp = (1/r) (W1 em1 + u (a + Bq))
+//   Ap (K3 wd + K4 wp) = (1/r^3) (dnx (t2 - u b) + a nn')
+// where t2 = a C + D, b = 3a + kr*kre (kernels.py:119-120), nn' = n.m'; the
+// sweep multiplies each stored acc2 partial by 1/Ap.
+// acc1 += K1 wd + K2 wp ; acc2 += Ap (K3 wd + K4 wp)   (solver.py:333-334)
+// 45 FP64 instructions per pair (24 DFMA, 14 DMUL, 7 DADD).
 template <bool FULL>
 __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, double nx, double ny,
                                               double nz, double sx, double sy, double sz, double mx,
                                               double my, double mz, double W1, double C, double D,
-                                              double Ap, double Bp, const double* __restrict__ etab,
+                                              double Bq, const double* __restrict__ etab,
                                               double& acc1, double& acc2) {
   double dx = tx - sx, dy = ty - sy, dz = tz - sz;
   double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
@@ -78,13 +81,13 @@ __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, d
   double kre = fma(r, em1, r);  // kr e^{-kr}
   double a = em1 + kre;         // (1+kr)e^{-kr} - 1      (kernels.py:119)
   double u = dny * ir2;
-  double t = fma(a, Ap, Bp);
+  double t = a + Bq;
   acc1 = fma(ir, fma(em1, W1, u * t), acc1);
   if (FULL) {
     double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
     double nn = fma(nx, mx, fma(ny, my, nz * mz));
     double b = fma(a, 3.0, r * kre);  // kernels.py:120
-    double g = fma(-u, b, fma(a, C, D));
+    double g = fma(a, C, fma(-u, b, D));
     double X = fma(dnx, g, a * nn);
     acc2 = fma(ir, X * ir2, acc2);
   }
@@ -99,7 +102,7 @@ template <int R>
 __device__ __forceinline__ void pairs_screened_stepmajor(
     const double (&tx)[R], const double (&ty)[R], const double (&tz)[R], const double (&nx)[R],
     const double (&ny)[R], const double (&nz)[R], double sx, double sy, double sz, double mx, double my,
-    double mz, double W1, double C, double D, double Ap, double Bp, const double* __restrict__ etab,
+    double mz, double W1, double C, double D, double Bq, const double* __restrict__ etab,
     double (&acc1)[R], double (&acc2)[R]) {
   double dx[R], dy[R], dz[R], r2[R], dny[R], dnx[R], nn[R], ir[R], r[R], em1[R], a[R], kre[R];
 #pragma unroll
@@ -143,7 +146,7 @@ __device__ __forceinline__ void pairs_screened_stepmajor(
     u[q] = dny[q] * ir2[q];
   }
 #pragma unroll
-  for (int q = 0; q < R; ++q) t[q] = fma(a[q], Ap, Bp);
+  for (int q = 0; q < R; ++q) t[q] = a[q] + Bq;
 #pragma unroll
   for (int q = 0; q < R; ++q) t[q] = u[q] * t[q];
 #pragma unroll
@@ -151,12 +154,12 @@ __device__ __forceinline__ void pairs_screened_stepmajor(
 #pragma unroll
   for (int q = 0; q < R; ++q) acc1[q] = fma(ir[q], t[q], acc1[q]);
 #pragma unroll
-  for (int q = 0; q < R; ++q) t[q] = fma(a[q], C, D);
-#pragma unroll
   for (int q = 0; q < R; ++q) {
     const double b = fma(a[q], 3.0, r[q] * kre[q]);
-    t[q] = fma(-u[q], b, t[q]);
+    t[q] = fma(-u[q], b, D);
   }
+#pragma unroll
+  for (int q = 0; q < R; ++q) t[q] = fma(a[q], C, t[q]);
 #pragma unroll
   for (int q = 0; q < R; ++q) nn[q] = a[q] * nn[q];
 #pragma unroll

@@ -106,7 +106,7 @@ template <int MODE, bool FULL, bool SELF, int R, int MINB, int UNROLL, bool STEP
 __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
     const double* __restrict__ tgt, int64_t ldt, int64_t t_begin, int64_t t_end,
     const double* __restrict__ src, const int2* __restrict__ groups, int n_groups,
-    double* __restrict__ part, int64_t ldp, unsigned* __restrict__ ticket, double Ap, double Bp) {
+    double* __restrict__ part, int64_t ldp, unsigned* __restrict__ ticket, double Bq, double s2) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
   double* etab = ring + kStages * kSrcTile * kSrcStride;
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
             const double2 p01 = rec[5 * j + 0], p2m0 = rec[5 * j + 1], m12 = rec[5 * j + 2];
             const double2 w01 = rec[5 * j + 3], w2x = rec[5 * j + 4];
             pairs_screened_stepmajor<R>(tx, ty, tz, nx, ny, nz, p01.x, p01.y, p2m0.x, p2m0.y, m12.x,
-                                        m12.y, w01.x, w01.y, w2x.x, Ap, Bp, etab, a1, a2);
+                                        m12.y, w01.x, w01.y, w2x.x, Bq, etab, a1, a2);
           }
         }
       }
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
             }
             if (MODE == kScreened)
               pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, mx, my, mz, W1,
-                                  C, D, Ap, Bp, etab, a1[q], a2[q]);
+                                  C, D, Bq, etab, a1[q], a2[q]);
             else
               pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, mx, my, mz, D,
                                  a1[q], a2[q]);
@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
       int64_t t = tb + q;
       if (t < t_end) {
         part[(2 * (int64_t)g) * ldp + t] = a1[q];
-        if (FULL) part[(2 * (int64_t)g + 1) * ldp + t] = a2[q];
+        // the screened record carries acc2 scaled by Ap = er/kappa (see
+        // weight_constants); s2 = 1/Ap undoes it once per row and item
+        if (FULL) part[(2 * (int64_t)g + 1) * ldp + t] = MODE == kScreened ? a2[q] * s2 : a2[q];
       }
     }
   }
@@ -576,21 +578,26 @@ constexpr int kWideVariant = 17;   // step_R6_minb2_unroll2: 768-row tiles, the 
 constexpr int kNarrowVariant = 15; // step_R4_minb3_unroll2: 512-row tiles
 static_assert(kWideVariant < kNumVariants && kNarrowVariant < kNumVariants, "variant table");
 
-// Physics folded into the per-source record and the launch constants Ap, Bp
-// (see hobi_fastmath.cuh).
+// Physics folded into the per-source record and two launch constants (see
+// hobi_fastmath.cuh).  Screened: with Ap = er/k, Bp = (er-1)/k the wp-weighted
+// normal carries M = Ap k^3 wp/4pi, so M' (a + Bq) with Bq = Bp/Ap is the K2
+// factor u (a Ap + Bp) of the unscaled record and the a*Ap DFMA becomes a DADD;
+// C and D carry the same Ap so the K3+K4 sum comes out scaled by Ap, undone by
+// s2 = 1/Ap when an item stores its row partials.
 struct WeightConstants {
-  double kM, kW1, kC, kD, Ap, Bp;
+  double kM, kW1, kC, kD, Bq, s2;
 };
 WeightConstants weight_constants(const Physics& p) {
   WeightConstants w{};
+  w.s2 = 1.0;
   if (p.mode == kScreened) {
-    const double k = p.kappa, k2 = k * k / kFourPi;
-    w.kM = k * k2;  // k^3/4pi
-    w.kW1 = -k / kFourPi;
-    w.kC = k2 / p.er;
-    w.kD = -k2 * (1.0 - 1.0 / p.er);
-    w.Ap = p.er / k;
-    w.Bp = (p.er - 1.0) / k;
+    const double k = p.kappa, k4 = k / kFourPi;
+    w.kM = k * k4 * p.er;             // Ap k^3/4pi = er k^2/4pi
+    w.kW1 = -k4;                      // -k/4pi
+    w.kC = k4;                        // Ap k^2/(4pi er) = k/4pi
+    w.kD = -k4 * (p.er - 1.0);        // -Ap k^2 (1-1/er)/4pi
+    w.Bq = (p.er - 1.0) / p.er;       // Bp/Ap
+    w.s2 = k / p.er;                  // 1/Ap
   } else {
     w.kM = (p.er - 1.0) / kFourPi;
     w.kD = -(1.0 - 1.0 / p.er) / kFourPi;
@@ -702,7 +709,7 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
         (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)std::max(per_sm, 1) * sms));
     HOBI_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
     sg.fn<<<grid, kSweepThreads, kSweepSmem, st>>>(tgt, ldt, sg.a, sg.b, c->src.p, groups, n_groups, part,
-                                                   ldp, ticket, wc.Ap, wc.Bp);
+                                                   ldp, ticket, wc.Bq, wc.s2);
     HOBI_CUDA(cudaGetLastError());
     c->launches++;
   }
