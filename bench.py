@@ -46,9 +46,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BIE matvec pair-interactions/s (FP64) and GMRES solve time at 1/2/4/8 B200"
 FLOPS_PER_PAIR = 96  # SURVEY.md 8(d) canonical accounting
-# FP64 instructions the default sweep executes per pair (24 DFMA + 14 DMUL + 7 DADD;
+# FP64 instructions the default sweep executes per pair (24 DFMA + 12 DMUL + 7 DADD;
 # SASS count, checked against the built library by tests/test_cabi.py)
-FP64_INSTR_PER_PAIR = 45
+FP64_INSTR_PER_PAIR = 43
 
 
 def _args():

@@ -929,20 +929,27 @@ int hobi_pairs_per_matvec(hobi_ctx* c, double* pairs) {
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// FP64 roofline probe: 8 independent DFMA chains per thread.
+// FP64 roofline probe: 8 independent DFMA chains per thread, each DFMA
+// reading two vector registers and one uniform register (the addend).  That
+// operand pattern issues at the FP64 pipe's full 64 lanes/clk/SM (measured
+// 63.5, the DMUL/DADD rate); a DFMA reading three vector registers without
+// reuse-cache hits runs at 2/3 of it, and x = fma(x, a, b) with a, b in
+// reused vector registers at ~58.6 (tools/fp64_probe2.cu, fp64_probe3.cu).
 
 namespace {
-__global__ void dfma_probe_kernel(double* out, int iters, double a, double b) {
-  double x0 = threadIdx.x * 1e-3, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
-  double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+__global__ void dfma_probe_kernel(double* out, int iters, double c) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = 0.5 + 1e-4 * k + 1e-7 * threadIdx.x;  // decays to ~c: no inf or subnormals
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
-      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
-    }
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fma(x[k], x[(k + 1) & 7], c);
   }
-  double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
   if (s == 123.456) out[0] = s;
 }
 }  // namespace
@@ -958,13 +965,13 @@ extern "C" int hobi_probe_fp64_tflops(int device, double ms, double* tflops) {
   EventPair ev;
   HOBI_CUDA(ev.create());
   cudaEvent_t e0 = ev.a, e1 = ev.b;
-  for (int w = 0; w < 3; ++w) dfma_probe_kernel<<<blocks, threads>>>(d.p, iters, 0.999999, 1e-7);
+  for (int w = 0; w < 3; ++w) dfma_probe_kernel<<<blocks, threads>>>(d.p, iters, 1e-9);
   HOBI_CUDA(cudaDeviceSynchronize());
   double total_ms = 0.0, flops = 0.0;
   float best = 1e30f;
   while (total_ms < ms) {
     HOBI_CUDA(cudaEventRecord(e0));
-    dfma_probe_kernel<<<blocks, threads>>>(d.p, iters, 0.999999, 1e-7);
+    dfma_probe_kernel<<<blocks, threads>>>(d.p, iters, 1e-9);
     HOBI_CUDA(cudaEventRecord(e1));
     HOBI_CUDA(cudaEventSynchronize(e1));
     float t = 0.f;

@@ -4,7 +4,7 @@
 // (1/4pi, kappa^n, er, 1/er) are folded into the per-source record (the wp
 // weight rides on the source normal) and two launch constants, expm1 and exp
 // share one table-driven range reduction, and 1/r comes from the MUFU rsqrt
-// seed plus one third-order Newton step.  45 FP64 instructions per pair
+// seed plus one third-order Newton step.  43 FP64 instructions per pair
 // (vs ~95 for a literal libdevice transcription of kernels.py:112-130).
 #pragma once
 
@@ -64,10 +64,12 @@ __device__ __forceinline__ double expm1_neg(double x, const double* __restrict__
 // where t2 = a C + D, b = 3a + kr*kre (kernels.py:119-120), nn' = n.m'; the
 // sweep multiplies each stored acc2 partial by 1/Ap.
 // acc1 += K1 wd + K2 wp ; acc2 += Ap (K3 wd + K4 wp)   (solver.py:333-334)
-// 45 FP64 instructions per pair (24 DFMA, 14 DMUL, 7 DADD).
+// Target normals come as (nx/nz, ny/nz) in the sweep frame (hobi_sweep.cu), so
+// d.n and n.m' need no leading DMUL; the sweep scales acc2 by nz per item.
+// 43 FP64 instructions per pair (24 DFMA, 12 DMUL, 7 DADD).
 template <bool FULL>
 __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, double nx, double ny,
-                                              double nz, double sx, double sy, double sz, double mx,
+                                              double sx, double sy, double sz, double mx,
                                               double my, double mz, double W1, double C, double D,
                                               double Bq, const double* __restrict__ etab,
                                               double& acc1, double& acc2) {
@@ -84,8 +86,8 @@ __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, d
   double t = a + Bq;
   acc1 = fma(ir, fma(em1, W1, u * t), acc1);
   if (FULL) {
-    double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
-    double nn = fma(nx, mx, fma(ny, my, nz * mz));
+    double dnx = fma(dx, nx, fma(dy, ny, dz));  // d.n / n_z (sweep frame)
+    double nn = fma(nx, mx, fma(ny, my, mz));   // n.m' / n_z
     double b = fma(a, 3.0, r * kre);  // kernels.py:120
     double g = fma(a, C, fma(-u, b, D));
     double X = fma(dnx, g, a * nn);
@@ -101,7 +103,7 @@ __device__ __forceinline__ void pair_screened(double tx, double ty, double tz, d
 template <int R>
 __device__ __forceinline__ void pairs_screened_stepmajor(
     const double (&tx)[R], const double (&ty)[R], const double (&tz)[R], const double (&nx)[R],
-    const double (&ny)[R], const double (&nz)[R], double sx, double sy, double sz, double mx, double my,
+    const double (&ny)[R], double sx, double sy, double sz, double mx, double my,
     double mz, double W1, double C, double D, double Bq, const double* __restrict__ etab,
     double (&acc1)[R], double (&acc2)[R]) {
   double dx[R], dy[R], dz[R], r2[R], dny[R], dnx[R], nn[R], ir[R], r[R], em1[R], a[R], kre[R];
@@ -120,13 +122,11 @@ __device__ __forceinline__ void pairs_screened_stepmajor(
 #pragma unroll
   for (int q = 0; q < R; ++q) dny[q] = fma(dx[q], mx, dny[q]);
 #pragma unroll
-  for (int q = 0; q < R; ++q) nn[q] = nz[q] * mz;
-#pragma unroll
-  for (int q = 0; q < R; ++q) nn[q] = fma(ny[q], my, nn[q]);
+  for (int q = 0; q < R; ++q) nn[q] = fma(ny[q], my, mz);
 #pragma unroll
   for (int q = 0; q < R; ++q) nn[q] = fma(nx[q], mx, nn[q]);
 #pragma unroll
-  for (int q = 0; q < R; ++q) dnx[q] = fma(dx[q], nx[q], fma(dy[q], ny[q], dz[q] * nz[q]));
+  for (int q = 0; q < R; ++q) dnx[q] = fma(dx[q], nx[q], fma(dy[q], ny[q], dz[q]));
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     ir[q] = rsqrt_fast(r2[q]);
@@ -173,7 +173,7 @@ __device__ __forceinline__ void pairs_screened_stepmajor(
 // (expm1(0) = 0 makes a = b = 0).  Record: m' = (er-1) wp/4pi m, D = -(1-1/er) wd/4pi.
 template <bool FULL>
 __device__ __forceinline__ void pair_laplace(double tx, double ty, double tz, double nx, double ny,
-                                             double nz, double sx, double sy, double sz, double mx,
+                                             double sx, double sy, double sz, double mx,
                                              double my, double mz, double D, double& acc1,
                                              double& acc2) {
   double dx = tx - sx, dy = ty - sy, dz = tz - sz;
@@ -183,7 +183,7 @@ __device__ __forceinline__ void pair_laplace(double tx, double ty, double tz, do
   double ir3 = (ir * ir) * ir;
   acc1 = fma(dny, ir3, acc1);
   if (FULL) {
-    double dnx = fma(dx, nx, fma(dy, ny, dz * nz));
+    double dnx = fma(dx, nx, fma(dy, ny, dz));  // d.n / n_z (sweep frame)
     acc2 = fma(dnx * ir3, D, acc2);
   }
 }

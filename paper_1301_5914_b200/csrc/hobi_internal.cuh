@@ -107,7 +107,22 @@ struct Physics {
   double diag1, diag2;  // 0.5*(1+er), 0.5*(1+1/er)  (solver.py:365-366)
   int mode;             // kLaplace when kappa == 0
   double len_scale;     // kappa for kScreened (coordinates are pre-scaled), 1 otherwise
+  // Sweep frame: a fixed rotation q (row-major) applied to every sweep
+  // position and normal, chosen so that no target normal has a zero (or
+  // subnormal) z component in it; the sweep then holds target normals as
+  // (nx/nz, ny/nz) and scales the K3+K4 row sum by nz once per item, which
+  // saves two DMULs per pair (hobi_fastmath.cuh).  Distances and dot products
+  // do not depend on the frame.
+  int frame = 0;
+  double q[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
 };
+
+// 3x3 matrix by value for kernel arguments.
+struct Mat3 {
+  double m[9];
+};
+constexpr int kNumFrames = 8;
+void set_frame(Physics& p, int k);  // rotation k of a fixed generic sequence
 
 struct Comm {
   void* nccl = nullptr;  // ncclComm_t

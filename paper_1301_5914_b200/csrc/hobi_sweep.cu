@@ -6,8 +6,9 @@
 // (kernels.py:99-130); solvation_energy (solver.py:581-614).
 //
 // Layout in HBM:
-//   tgt  : SoA (6, nt_pad)  x', y', z', nx, ny, nz   (x' = len_scale * x)
-//   src  : AoS (ns_pad, 10) x', y', z', M nx, M ny, M nz, W1, C, D, 0
+//   tgt  : SoA (6, nt_pad)  x', y', z', nx'/nz', ny'/nz', nz'
+//          (x' = len_scale * Q x, n' = Q n: the sweep frame, Physics::q)
+//   src  : AoS (ns_pad, 10) x', y', z', M n'x, M n'y, M n'z, W1, C, D, 0
 //          (M = k^3 wp/4pi screened, (er-1) wp/4pi unscreened; hobi_fastmath.cuh)
 //   part : (n_groups, 2, nt_pad) per-source-group partial sums
 // The sweep is persistent: each resident CTA pulls work items (a tile of
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
                  kTileBytes, &bars[st]);
       }
     }
-    double tx[R], ty[R], tz[R], nx[R], ny[R], nz[R];
+    double tx[R], ty[R], tz[R], nx[R], ny[R];  // normals as (n'x/n'z, n'y/n'z)
     double a1[R], a2[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
@@ -158,7 +159,6 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
       tz[q] = tgt[2 * ldt + t];
       nx[q] = tgt[3 * ldt + t];
       ny[q] = tgt[4 * ldt + t];
-      nz[q] = tgt[5 * ldt + t];
       a1[q] = 0.0;
       a2[q] = 0.0;
     }
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
           for (int j = 0; j < (warp_live ? kSrcTile : 0); ++j) {
             const double2 p01 = rec[5 * j + 0], p2m0 = rec[5 * j + 1], m12 = rec[5 * j + 2];
             const double2 w01 = rec[5 * j + 3], w2x = rec[5 * j + 4];
-            pairs_screened_stepmajor<R>(tx, ty, tz, nx, ny, nz, p01.x, p01.y, p2m0.x, p2m0.y, m12.x,
+            pairs_screened_stepmajor<R>(tx, ty, tz, nx, ny, p01.x, p01.y, p2m0.x, p2m0.y, m12.x,
                                         m12.y, w01.x, w01.y, w2x.x, Bq, etab, a1, a2);
           }
         }
@@ -219,10 +219,10 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
               }
             }
             if (MODE == kScreened)
-              pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, mx, my, mz, W1,
+              pair_screened<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], sx, sy, sz, mx, my, mz, W1,
                                   C, D, Bq, etab, a1[q], a2[q]);
             else
-              pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], nz[q], sx, sy, sz, mx, my, mz, D,
+              pair_laplace<FULL>(tx[q], ty[q], tz[q], nx[q], ny[q], sx, sy, sz, mx, my, mz, D,
                                  a1[q], a2[q]);
           }
         }
@@ -235,9 +235,10 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
       int64_t t = tb + q;
       if (t < t_end) {
         part[(2 * (int64_t)g) * ldp + t] = a1[q];
-        // the screened record carries acc2 scaled by Ap = er/kappa (see
-        // weight_constants); s2 = 1/Ap undoes it once per row and item
-        if (FULL) part[(2 * (int64_t)g + 1) * ldp + t] = MODE == kScreened ? a2[q] * s2 : a2[q];
+        // acc2 accumulated d.n/n'z terms (the sweep frame) and, screened, a
+        // record scaled by Ap = er/kappa (weight_constants): one multiply by
+        // n'z * s2 per row and item restores the K3+K4 sum
+        if (FULL) part[(2 * (int64_t)g + 1) * ldp + t] = a2[q] * (tgt[5 * ldt + t] * s2);
       }
     }
   }
@@ -245,15 +246,20 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
 
 // Scaled static source positions: record fields 0..2; padding records get
 // zero weights (fields 3..9), so they contribute exactly +-0.
+__device__ __forceinline__ double row3(const Mat3& a, int i, double x, double y, double z) {
+  return fma(a.m[3 * i], x, fma(a.m[3 * i + 1], y, a.m[3 * i + 2] * z));
+}
+
 __global__ void static_sources_kernel(const double* __restrict__ pos, int64_t ns, int64_t ns_pad,
-                                      double scale, double* __restrict__ src) {
+                                      Mat3 sq, double* __restrict__ src) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= ns_pad) return;
   double* rec = src + s * kSrcStride;
-  if (s < ns) {
-    rec[0] = scale * pos[3 * s];
-    rec[1] = scale * pos[3 * s + 1];
-    rec[2] = scale * pos[3 * s + 2];
+  if (s < ns) {  // x' = (len_scale Q) x
+    const double x = pos[3 * s], y = pos[3 * s + 1], z = pos[3 * s + 2];
+    rec[0] = row3(sq, 0, x, y, z);
+    rec[1] = row3(sq, 1, x, y, z);
+    rec[2] = row3(sq, 2, x, y, z);
   } else {  // padding: far away
     rec[0] = 1e6 + (double)(s - ns);
     rec[1] = 1e6;
@@ -262,18 +268,34 @@ __global__ void static_sources_kernel(const double* __restrict__ pos, int64_t ns
   for (int k = 3; k < kSrcStride; ++k) rec[k] = 0.0;
 }
 
-// Targets SoA, scaled.
+// Targets SoA in the sweep frame: x' = (len_scale Q) x, n' = Q n stored as
+// (n'x/n'z, n'y/n'z, n'z).  A target whose n'z is zero or below 1e-150 in
+// magnitude sets *bad (the caller then picks the next frame).  Charges (no
+// normal) get n' = (0, 0, 1).
 __global__ void targets_kernel(const double* __restrict__ pos, const double* __restrict__ nrm,
-                               int64_t nt, int64_t ldt, double scale, double* __restrict__ tgt) {
+                               int64_t nt, int64_t ldt, Mat3 sq, Mat3 q, double* __restrict__ tgt,
+                               int* __restrict__ bad) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ldt) return;
   int64_t i = t < nt ? t : nt - 1;
-  tgt[t] = scale * pos[3 * i];
-  tgt[ldt + t] = scale * pos[3 * i + 1];
-  tgt[2 * ldt + t] = scale * pos[3 * i + 2];
-  tgt[3 * ldt + t] = nrm ? nrm[3 * i] : 1.0;
-  tgt[4 * ldt + t] = nrm ? nrm[3 * i + 1] : 0.0;
-  tgt[5 * ldt + t] = nrm ? nrm[3 * i + 2] : 0.0;
+  const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+  tgt[t] = row3(sq, 0, x, y, z);
+  tgt[ldt + t] = row3(sq, 1, x, y, z);
+  tgt[2 * ldt + t] = row3(sq, 2, x, y, z);
+  double px = 0.0, py = 0.0, nz = 1.0;
+  if (nrm) {
+    const double a = nrm[3 * i], b = nrm[3 * i + 1], c = nrm[3 * i + 2];
+    nz = row3(q, 2, a, b, c);
+    if (!(fabs(nz) >= 1e-150)) {
+      if (bad) atomicExch(bad, 1);
+      nz = 1.0;
+    }
+    px = row3(q, 0, a, b, c) / nz;
+    py = row3(q, 1, a, b, c) / nz;
+  }
+  tgt[3 * ldt + t] = px;
+  tgt[4 * ldt + t] = py;
+  tgt[5 * ldt + t] = nz;
 }
 
 // K-C: interpolate u onto the regular points and fold the physics into the
@@ -284,7 +306,7 @@ __global__ void source_weights_kernel(const double* __restrict__ u, int64_t nt,
                                       const int* __restrict__ faces, const double* __restrict__ reg_w,
                                       const double* __restrict__ bary, int nq, int64_t ns,
                                       const double* __restrict__ area, const double* __restrict__ nrm,
-                                      double kM, double kW1, double kC, double kD,
+                                      double kM, double kW1, double kC, double kD, Mat3 q,
                                       double* __restrict__ src) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= ns) return;
@@ -306,9 +328,10 @@ __global__ void source_weights_kernel(const double* __restrict__ u, int64_t nt,
   }
   double* rec = src + s * kSrcStride;
   const double M = kM * wp;
-  rec[3] = M * nrm[3 * s];
-  rec[4] = M * nrm[3 * s + 1];
-  rec[5] = M * nrm[3 * s + 2];
+  const double a = nrm[3 * s], b = nrm[3 * s + 1], c = nrm[3 * s + 2];
+  rec[3] = M * row3(q, 0, a, b, c);  // weighted normal in the sweep frame
+  rec[4] = M * row3(q, 1, a, b, c);
+  rec[5] = M * row3(q, 2, a, b, c);
   rec[6] = kW1 * wd;
   rec[7] = kC * wd;
   rec[8] = kD * wd;
@@ -768,19 +791,55 @@ int sweep_variant_count() { return kNumVariants; }
 const char* sweep_variant_name(int v) { return (v >= 0 && v < kNumVariants) ? kVariants[v].name : ""; }
 
 
+// Rotation k of a fixed sequence of generic frames (Rodrigues; axis and angle
+// chosen away from the coordinate planes that icosphere and MSMS meshes tend
+// to populate with exactly zero normal components).
+void set_frame(Physics& p, int k) {
+  const double ax = 1.0, ay = 1.0 + 0.37 * k, az = 1.61 + 0.23 * k;
+  const double n = std::sqrt(ax * ax + ay * ay + az * az);
+  const double x = ax / n, y = ay / n, z = az / n;
+  const double th = 0.0625 * (1.0 + 0.5 * k), co = std::cos(th), si = std::sin(th), t = 1.0 - co;
+  const double q[9] = {t * x * x + co,     t * x * y - si * z, t * x * z + si * y,
+                       t * x * y + si * z, t * y * y + co,     t * y * z - si * x,
+                       t * x * z - si * y, t * y * z + si * x, t * z * z + co};
+  p.frame = k;
+  for (int i = 0; i < 9; ++i) p.q[i] = q[i];
+}
+
+static Mat3 frame_rot(const Physics& p) {
+  Mat3 m;
+  for (int i = 0; i < 9; ++i) m.m[i] = p.q[i];
+  return m;
+}
+static Mat3 frame_pos(const Physics& p) {  // len_scale * Q for positions
+  Mat3 m;
+  for (int i = 0; i < 9; ++i) m.m[i] = p.len_scale * p.q[i];
+  return m;
+}
+
 int prepare_targets(hobi_ctx* c) {
   const double* pos = c->scheme == kHobi ? c->vert.p : c->reg_pos.p;  // lobi: centroids
   const double* nrm = c->scheme == kHobi ? c->vnrm.p : c->reg_nrm.p;
-  targets_kernel<<<nblk(c->nt_pad, 256), 256, 0, c->stream>>>(pos, nrm, c->nt, c->nt_pad,
-                                                              c->phys.len_scale, c->tgt.p);
-  c->launches++;
-  HOBI_CUDA(cudaGetLastError());
-  return 0;
+  DevBuf<int> bad;
+  if (bad.alloc(1)) return HOBI_ERR_CUDA;
+  for (int k = c->phys.frame; k < kNumFrames; ++k) {
+    set_frame(c->phys, k);
+    HOBI_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+    targets_kernel<<<nblk(c->nt_pad, 256), 256, 0, c->stream>>>(
+        pos, nrm, c->nt, c->nt_pad, frame_pos(c->phys), frame_rot(c->phys), c->tgt.p, bad.p);
+    c->launches++;
+    HOBI_CUDA(cudaGetLastError());
+    int h = 0;
+    HOBI_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    HOBI_CUDA(cudaStreamSynchronize(c->stream));
+    if (!h) return 0;
+  }
+  return fail(HOBI_ERR_VALUE, "no sweep frame gives every collocation normal a nonzero z component");
 }
 
 int prepare_static_sources(hobi_ctx* c) {
   static_sources_kernel<<<nblk(c->ns_pad, 256), 256, 0, c->stream>>>(
-      c->reg_pos.p, c->ns, c->ns_pad, c->phys.len_scale, c->src.p);
+      c->reg_pos.p, c->ns, c->ns_pad, frame_pos(c->phys), c->src.p);
   c->launches++;
   HOBI_CUDA(cudaGetLastError());
   return 0;
@@ -790,7 +849,8 @@ static int update_weights(hobi_ctx* c, const double* u_dev) {
   const WeightConstants w = weight_constants(c->phys);
   source_weights_kernel<<<nblk(c->ns, 256), 256, 0, c->stream>>>(
       u_dev, c->nt, c->faces.p, c->reg_w.p, c->reg_bary.p, c->nq, c->ns,
-      c->scheme == kLobi ? c->lobi_area.p : nullptr, c->reg_nrm.p, w.kM, w.kW1, w.kC, w.kD, c->src.p);
+      c->scheme == kLobi ? c->lobi_area.p : nullptr, c->reg_nrm.p, w.kM, w.kW1, w.kC, w.kD,
+      frame_rot(c->phys), c->src.p);
   c->launches++;
   HOBI_CUDA(cudaGetLastError());
   return 0;
@@ -915,8 +975,8 @@ int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, 
   HOBI_CUDA(cudaMemcpyAsync(w.qpos.p, qpos, 3 * nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   double *tq = w.tq.p, *part = w.part.p, *dq = w.q.p;
   const int2* dgroups = w.groups.p;
-  targets_kernel<<<nblk(ldc, 256), 256, 0, c->stream>>>(w.qpos.p, nullptr, nc, ldc,
-                                                        c->phys.len_scale, tq);
+  targets_kernel<<<nblk(ldc, 256), 256, 0, c->stream>>>(w.qpos.p, nullptr, nc, ldc, frame_pos(c->phys),
+                                                        frame_rot(c->phys), tq, nullptr);
   c->launches++;
   if ((rc = update_weights(c, x_dev))) return rc;
   // Under a communicator the charges are split across ranks; the per-charge

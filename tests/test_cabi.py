@@ -46,7 +46,7 @@ def test_library_is_sm100a_only():
 
 
 def test_default_sweep_executes_the_documented_instruction_mix():
-    """bench.py's FP64_INSTR_PER_PAIR and DESIGN.md's 24 DFMA + 14 DMUL + 7 DADD
+    """bench.py's FP64_INSTR_PER_PAIR and DESIGN.md's 24 DFMA + 12 DMUL + 7 DADD
     are the SASS of the default sweep variants: step_R6_minb2_unroll2 (6
     targets x 2 unrolled sources = 12 pairs per loop body, nothing else FP64)
     and step_R4_minb3_unroll2 (8 pairs), used when a row range leaves a long
@@ -71,9 +71,9 @@ def test_default_sweep_executes_the_documented_instruction_mix():
                 body.append(line)
         sass = "\n".join(body)
         counts = {op: len(re.findall(r"\b" + op + r"\b", sass)) for op in ("DFMA", "DMUL", "DADD")}
-        # + one DMUL per target row when an item stores its acc2 partial (the 1/Ap scale)
-        assert counts == {"DFMA": 24 * pairs, "DMUL": 14 * pairs + r, "DADD": 7 * pairs}, (frag, counts)
-    assert bench.FP64_INSTR_PER_PAIR == 45
+        # + two DMULs per target row when an item stores its acc2 partial (the n'z / Ap scale)
+        assert counts == {"DFMA": 24 * pairs, "DMUL": 12 * pairs + 2 * r, "DADD": 7 * pairs}, (frag, counts)
+    assert bench.FP64_INSTR_PER_PAIR == 43
 
 
 def test_no_cpu_fallback_without_device():
