@@ -154,6 +154,11 @@ static int common_init(hobi_ctx* c, int device, double eps1, double eps2, double
   p.diag2 = 0.5 * (1.0 + 1.0 / p.er);
   p.mode = kappa > 0.0 ? kScreened : kLaplace;
   p.len_scale = p.mode == kScreened ? kappa : 1.0;
+  if (const char* f = getenv("HOBI_SWEEP_FRAME")) {  // testing: first sweep frame tried
+    const int k = atoi(f);
+    if (k < 0 || k >= kNumFrames) return fail(HOBI_ERR_VALUE, "HOBI_SWEEP_FRAME out of range");
+    p.frame = k;
+  }
   int rc;
   if ((rc = upload_exp_table())) return rc;
   return 0;

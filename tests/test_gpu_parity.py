@@ -31,6 +31,7 @@ from paper_1301_5914_b200 import (  # noqa: E402
     solvation_energy,
     solve,
 )
+from paper_1301_5914_b200.solver import SurfaceSolution  # noqa: E402
 from paper_1301_5914_b200 import _native as N  # noqa: E402
 
 MATVEC_TOL = 1e-12
@@ -370,6 +371,28 @@ def test_repeated_runs_and_all_sweep_variants_bitwise_identical():
     for v in range(n.value):
         N.check(lib.hobi_sweep_variant(prob.handle, v, None, None, 0))
         assert np.array_equal(matvec_hobi(prob, g["u"]), ref), v
+
+
+def test_sweep_frame_invariance(monkeypatch):
+    """The sweep runs in a rotated frame with target normals held as
+    (n_x/n_z, n_y/n_z) (csrc/hobi_sweep.cu, Physics::q).  Distances and dot
+    products do not depend on the frame: the matvec and the energy computed in
+    different frames of the sequence agree to rounding, and each matches the
+    reference golden."""
+    g = golden("star_l3")
+    out = []
+    for k in (0, 3, 7):
+        monkeypatch.setenv("HOBI_SWEEP_FRAME", str(k))
+        prob = _problem(g)
+        au = matvec_hobi(prob, g["u"])
+        assert np.linalg.norm(au - g["Au"]) / np.linalg.norm(g["Au"]) <= 1e-12, k
+        sol = SurfaceSolution(np.asarray(g["phi"], float), np.asarray(g["dphi"], float), "hobi", 0, 0.0)
+        assert abs(solvation_energy(prob, sol) - float(g["energy"])) <= 1e-10 * abs(float(g["energy"]))
+        out.append((au, solvation_energy(prob, sol)))
+        prob.close()
+    for au, e in out[1:]:
+        assert np.linalg.norm(au - out[0][0]) / np.linalg.norm(out[0][0]) <= 1e-14
+        assert abs(e - out[0][1]) <= 1e-13 * abs(out[0][1])
 
 
 def test_elements_are_the_rotation0_nodes():
