@@ -23,8 +23,8 @@
 // K1/K2-only energy sweep), SELF (LOBI self-pair mask, applied only on source
 // tiles that overlap the item's rows), R targets per thread, MINB CTAs per SM,
 // UNROLL of the source loop, STEP (step-major pair arithmetic).  launch_sweep
-// picks a 768-row tile, falls back to 512-row tiles for ranges with a long
-// remainder and to 128-row tiles for small ranges, and runs the rows past the
+// picks a 768-row or a 512-row tile (whichever leaves fewer rows past the last
+// whole tile), falls back to 128-row tiles for small ranges, and runs the rows past the
 // last whole tile as a second 128-row-tile launch on the side stream.
 #include <algorithm>
 #include <cmath>
@@ -665,14 +665,16 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
                 small = tuned ? kSmallVariant : 2;
       int vi = tuned ? c->sweep_variant : wide;
       const bool pinned = c->variant_pinned && tuned;
-      // the wide tile is ~1% faster per pair, but a range that leaves more
-      // than 2% of its rows past the last whole 768-row tile (an 8-way split
-      // of config 4 leaves 513 of 5121) runs better on 512-row tiles
+      // the two tiles run at the same rate per pair, but the rows past the
+      // last whole tile cost more than their share (a side launch of
+      // 128-row tiles that mostly runs after the persistent main launch):
+      // take the tile that leaves fewer of them (config 4 leaves 258 rows
+      // past 768-row tiles and 2 past 512-row tiles; an 8-way split 513 vs 1)
       if (!pinned && vi == wide) {
         const int64_t rows = t1 - t0;
         const int64_t rem_w = rows % (kSweepThreads * tab[wide].r);
         const int64_t rem_n = rows % (kSweepThreads * tab[narrow].r);
-        if (rem_w * 50 > rows && rem_n < rem_w) vi = narrow;
+        if (rem_n < rem_w) vi = narrow;
       }
       // small problems: if the tuned tile leaves too few work items for 148
       // SMs, use 128-row tiles (same sums bitwise, more parallelism)
