@@ -665,16 +665,18 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
                 small = tuned ? kSmallVariant : 2;
       int vi = tuned ? c->sweep_variant : wide;
       const bool pinned = c->variant_pinned && tuned;
-      // the two tiles run at the same rate per pair, but the rows past the
-      // last whole tile cost more than their share (a side launch of
-      // 128-row tiles that mostly runs after the persistent main launch):
-      // take the tile that leaves fewer of them (config 4 leaves 258 rows
-      // past 768-row tiles and 2 past 512-row tiles; an 8-way split 513 vs 1)
+      // the rows past the last whole tile cost more than their share (a side
+      // launch of 128-row tiles that mostly runs after the persistent main
+      // launch).  The tuned screened tiles run at the same rate per pair:
+      // take the one that leaves fewer remainder rows (config 4 leaves 258
+      // past 768-row tiles and 2 past 512-row tiles; an 8-way split 513 vs 1).
+      // The other instantiations' narrow tile is slower per pair (LOBI 1.7%):
+      // switch only when the wide tile would leave more than 2% of the rows.
       if (!pinned && vi == wide) {
         const int64_t rows = t1 - t0;
         const int64_t rem_w = rows % (kSweepThreads * tab[wide].r);
         const int64_t rem_n = rows % (kSweepThreads * tab[narrow].r);
-        if (rem_n < rem_w) vi = narrow;
+        if (rem_n < rem_w && (tuned || rem_w * 50 > rows)) vi = narrow;
       }
       // small problems: if the tuned tile leaves too few work items for 148
       // SMs, use 128-row tiles (same sums bitwise, more parallelism)
