@@ -135,8 +135,10 @@ static int common_init(hobi_ctx* c, int device, double eps1, double eps2, double
   HOBI_CUDA(cudaSetDevice(device));
   HOBI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   HOBI_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  HOBI_CUDA(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));
   HOBI_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   HOBI_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+  HOBI_CUDA(cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming));
   HOBI_CUDA(cudaEventCreate(&c->ev0));
   HOBI_CUDA(cudaEventCreate(&c->ev1));
   if (const char* v = getenv("HOBI_SWEEP_VARIANT")) {  // tuning: default tile, still auto-switched
@@ -510,12 +512,15 @@ int hobi_destroy(hobi_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->side) cudaStreamSynchronize(c->side);
+  if (c->side2) cudaStreamSynchronize(c->side2);
   if (c->fork) cudaEventDestroy(c->fork);
   if (c->join) cudaEventDestroy(c->join);
-  cudaStream_t s = c->stream, side = c->side;
+  if (c->join2) cudaEventDestroy(c->join2);
+  cudaStream_t s = c->stream, side = c->side, side2 = c->side2;
   delete c;  // DevBufs free themselves
   if (s) cudaStreamDestroy(s);
   if (side) cudaStreamDestroy(side);
+  if (side2) cudaStreamDestroy(side2);
   return 0;
 }
 

@@ -159,7 +159,8 @@ struct hobi_ctx {
   int scheme = hobi::kHobi;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;              // Duffy swap runs here, concurrent with the sweep
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t side2 = nullptr;             // rows past the last whole sweep tile, concurrent too
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
   hobi::Physics phys{};
   int64_t nv = 0, nf = 0;  // mesh sizes
   int64_t nt = 0;          // collocation points (targets)
