@@ -834,6 +834,9 @@ int prepare_targets(hobi_ctx* c) {
   const double* nrm = c->scheme == kHobi ? c->vnrm.p : c->reg_nrm.p;
   DevBuf<int> bad;
   if (bad.alloc(1)) return HOBI_ERR_CUDA;
+  // test hook: frames below this index count as rejected (exercises the retry)
+  const char* rej = getenv("HOBI_TEST_FRAME_REJECT");
+  const int reject_below = rej ? atoi(rej) : 0;
   for (int k = c->phys.frame; k < kNumFrames; ++k) {
     set_frame(c->phys, k);
     HOBI_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
@@ -844,7 +847,7 @@ int prepare_targets(hobi_ctx* c) {
     int h = 0;
     HOBI_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     HOBI_CUDA(cudaStreamSynchronize(c->stream));
-    if (!h) return 0;
+    if (!h && k >= reject_below) return 0;
   }
   return fail(HOBI_ERR_VALUE, "no sweep frame gives every collocation normal a nonzero z component");
 }

@@ -395,6 +395,23 @@ def test_sweep_frame_invariance(monkeypatch):
         assert abs(e - out[0][1]) <= 1e-13 * abs(out[0][1])
 
 
+def test_sweep_frame_retry(monkeypatch):
+    """Context creation tries the frames of the sequence until every target
+    normal has a nonzero z component (csrc/hobi_sweep.cu prepare_targets);
+    the HOBI_TEST_FRAME_REJECT hook rejects the first frames: the retry lands
+    on a later frame with the same results, and rejecting all of them is a
+    clean error, not a wrong answer."""
+    g = golden("star_l3")
+    monkeypatch.setenv("HOBI_TEST_FRAME_REJECT", "5")
+    prob = _problem(g)
+    au = matvec_hobi(prob, g["u"])
+    assert np.linalg.norm(au - g["Au"]) / np.linalg.norm(g["Au"]) <= 1e-12
+    prob.close()
+    monkeypatch.setenv("HOBI_TEST_FRAME_REJECT", "8")
+    with pytest.raises(Exception, match="no sweep frame"):
+        _problem(g)
+
+
 def test_elements_are_the_rotation0_nodes():
     """problem.elements (solver.py:208-215): node 0/3/8 are the face's vertices bitwise."""
     g = golden("star_l2")
