@@ -1,5 +1,6 @@
 """One-off parity evidence at BASELINE config 3 (L5 star surface, 20,480
-curved triangles, 500 charges, restart 20, tol 1e-6): the full GPU solve
+curved triangles, 500 charges, restart 20, tol 1e-6; `python
+tests/checks/c3_solve_check.py 4` runs config 4, about an hour of oracle time): the full GPU solve
 through the public API against a full oracle solve (the reference algorithm
 restated in numpy, fork pool over all host cores) on the same seeded inputs —
 GMRES iteration and matvec counts, surface potential, normal derivative and
@@ -16,7 +17,7 @@ import hobi_oracle as O  # noqa: E402
 from paper_1301_5914_b200 import PhysicalParams, SolverConfig, solvation_energy, solve  # noqa: E402
 from paper_1301_5914_b200.surfaces import baseline_config  # noqa: E402
 
-cfg = baseline_config(3)
+cfg = baseline_config(int(sys.argv[1]) if len(sys.argv) > 1 else 3)
 m = cfg.mesh
 t0 = time.time()
 prob, sol = solve(m, PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa), cfg.charges,
