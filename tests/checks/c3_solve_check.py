@@ -18,17 +18,18 @@ from paper_1301_5914_b200 import PhysicalParams, SolverConfig, solvation_energy,
 from paper_1301_5914_b200.surfaces import baseline_config  # noqa: E402
 
 cfg = baseline_config(int(sys.argv[1]) if len(sys.argv) > 1 else 3)
+scheme = sys.argv[2] if len(sys.argv) > 2 else "hobi"  # "lobi": the flat one-point scheme (f1)
 m = cfg.mesh
 t0 = time.time()
 prob, sol = solve(m, PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa), cfg.charges,
-                  SolverConfig(workers=1, restart=cfg.restart, tolerance=cfg.tol))
+                  SolverConfig(workers=1, restart=cfg.restart, tolerance=cfg.tol, scheme=scheme))
 e_gpu = solvation_energy(prob, sol)
 t_gpu = time.time() - t0
-print(f"GPU solve: {sol.iterations} its, residual {sol.residual:.3e}, E {e_gpu:.12f} kcal/mol, {t_gpu:.2f} s",
+print(f"scheme {scheme}: GPU solve: {sol.iterations} its, residual {sol.residual:.3e}, E {e_gpu:.12f} kcal/mol, {t_gpu:.2f} s",
       flush=True)
 t0 = time.time()
 o = O.discretize(m.vertices, m.normals, m.faces, cfg.eps1, cfg.eps2, cfg.kappa,
-                 cfg.charges.positions, cfg.charges.charges, check=False)
+                 cfg.charges.positions, cfg.charges.charges, scheme=scheme, check=False)
 workers = os.cpu_count() or 1
 phi, dphi, its, rel, nmv = O.solve(o, tol=cfg.tol, restart=cfg.restart, workers=workers)
 e_ref = O.energy(o, phi, dphi)
