@@ -214,7 +214,7 @@ struct hobi_ctx {
   int64_t sweep_launches = 0;
   int64_t launches = 0;
   bool timing = true;
-  int sweep_variant = 21;  // index into the sweep tuning table (hobi_sweep.cu): step_R6_minb2_unroll3
+  int sweep_variant = 22;  // index into the sweep tuning table (hobi_sweep.cu): step_R7_minb2_unroll3
   bool variant_pinned = false;  // set by hobi_sweep_variant: no small-problem switch
   hobi::GmresWorkspace gmres_ws;
   hobi::ChargeWorkspace charge_ws;

@@ -562,7 +562,7 @@ static const SweepVariant kVariants[] = {
     HOBI_V(4, 4, 1), HOBI_V(3, 4, 1), HOBI_V(6, 2, 1), HOBI_V(8, 2, 1), HOBI_V(3, 4, 2),
     HOBI_V(4, 4, 2), HOBI_V(5, 3, 1), HOBI_VS(6, 2, 1), HOBI_VS(4, 3, 1), HOBI_VS(3, 4, 1),
     HOBI_VS(4, 3, 2), HOBI_VS(4, 3, 4), HOBI_VS(6, 2, 2), HOBI_VS(3, 4, 2), HOBI_VS(5, 3, 2),
-    HOBI_VS(8, 2, 2), HOBI_VS(6, 2, 3),
+    HOBI_VS(8, 2, 2), HOBI_VS(6, 2, 3), HOBI_VS(7, 2, 3),
 };
 #undef HOBI_V
 #undef HOBI_VS
@@ -597,7 +597,7 @@ static const SweepVariant kLaplaceSelfVariants[] = {
     {sweep_kernel<kLaplace, true, true, 1, 6, 2>, 1, "laplace_self_R1_minb6_unroll2"},
 };
 constexpr int kSmallVariant = 3;   // R1_minb8_unroll2
-constexpr int kWideVariant = 21;   // step_R6_minb2_unroll3: 768-row tiles, the default
+constexpr int kWideVariant = 22;   // step_R7_minb2_unroll3: 896-row tiles, the default
 constexpr int kNarrowVariant = 15; // step_R4_minb3_unroll2: 512-row tiles
 static_assert(kWideVariant < kNumVariants && kNarrowVariant < kNumVariants, "variant table");
 
@@ -665,17 +665,18 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
                 small = tuned ? kSmallVariant : 2;
       int vi = tuned ? c->sweep_variant : wide;
       const bool pinned = c->variant_pinned && tuned;
-      // the wide tile is ~0.5% faster per pair, but the rows past the last
+      // the wide tile is ~2% faster per pair, but the rows past the last
       // whole tile cost more than their share (a side launch of 128-row
       // tiles beside the persistent main launch): switch to the narrow tile
-      // when the wide one would leave more than 2% of the rows and the narrow
-      // one fewer (config 4 keeps 768-row tiles and 258 remainder rows; its
-      // 2/4/8-way splits leave 513/257/513 rows vs 1 and switch).
+      // when the wide one would leave more than 5% of the rows and the narrow
+      // one fewer (config 4 keeps 896-row tiles and 642 remainder rows, as
+      // do its 2- and 4-way splits; the 8-way split leaves 641 of 5,121 rows
+      // vs 1 and switches).
       if (!pinned && vi == wide) {
         const int64_t rows = t1 - t0;
         const int64_t rem_w = rows % (kSweepThreads * tab[wide].r);
         const int64_t rem_n = rows % (kSweepThreads * tab[narrow].r);
-        if (rem_n < rem_w && rem_w * 50 > rows) vi = narrow;
+        if (rem_n < rem_w && rem_w * 20 > rows) vi = narrow;
       }
       // small problems: if the tuned tile leaves too few work items for 148
       // SMs, use 128-row tiles (same sums bitwise, more parallelism)

@@ -47,8 +47,8 @@ def test_library_is_sm100a_only():
 
 def test_default_sweep_executes_the_documented_instruction_mix():
     """bench.py's FP64_INSTR_PER_PAIR and DESIGN.md's 24 DFMA + 12 DMUL + 7 DADD
-    are the SASS of the default sweep variants: step_R6_minb2_unroll3 (6
-    targets x 3 unrolled sources = 18 pairs per loop body, nothing else FP64)
+    are the SASS of the default sweep variants: step_R7_minb2_unroll3 (7
+    targets x 3 unrolled sources = 21 pairs per loop body, nothing else FP64)
     and step_R4_minb3_unroll2 (8 pairs), used when a row range leaves a long
     remainder past the 768-row tiles."""
     import subprocess
@@ -56,13 +56,13 @@ def test_default_sweep_executes_the_documented_instruction_mix():
     import bench
 
     internal = open(os.path.join(ROOT, "paper_1301_5914_b200", "csrc", "hobi_internal.cuh")).read()
-    assert re.search(r"int sweep_variant = 21;.*step_R6_minb2_unroll3", internal)
+    assert re.search(r"int sweep_variant = 22;.*step_R7_minb2_unroll3", internal)
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", N.LIB_PATH], capture_output=True,
                          text=True)
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
-    # unroll 3 over 64-source tiles: an 18-pair loop body plus a 6-pair tail (24 in the function)
-    for frag, pairs, r in (("sweep_kernelILi1ELb1ELb0ELi6ELi2ELi3ELb1E", 24, 6),
+    # unroll 3 over 64-source tiles: a 21-pair loop body plus a 7-pair tail (28 in the function)
+    for frag, pairs, r in (("sweep_kernelILi1ELb1ELb0ELi7ELi2ELi3ELb1E", 28, 7),
                            ("sweep_kernelILi1ELb1ELb0ELi4ELi3ELi2ELb1E", 8, 4)):
         body, on = [], False
         for line in out.stdout.splitlines():
