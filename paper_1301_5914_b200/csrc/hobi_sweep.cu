@@ -569,30 +569,30 @@ static const SweepVariant kVariants[] = {
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 // LOBI (self-pair mask) counterparts of the wide / narrow / small tiles.
 static const SweepVariant kSelfVariants[] = {
-    {sweep_kernel<kScreened, true, true, 6, 2, 2, true>, 6, "self_step_R6_minb2_unroll2"},
+    {sweep_kernel<kScreened, true, true, 7, 2, 3, true>, 7, "self_step_R7_minb2_unroll3"},
     {sweep_kernel<kScreened, true, true, 4, 3, 2, true>, 4, "self_step_R4_minb3_unroll2"},
     {sweep_kernel<kScreened, true, true, 1, 6, 2>, 1, "self_R1_minb6_unroll2"},
 };
 // kappa = 0 (Laplace instantiation, no step-major form needed): wide / narrow
 // / small tiles, without and with the LOBI self mask.
 static const SweepVariant kLaplaceVariants[] = {
-    {sweep_kernel<kLaplace, true, false, 6, 2, 2>, 6, "laplace_R6_minb2_unroll2"},
+    {sweep_kernel<kLaplace, true, false, 7, 2, 3>, 7, "laplace_R7_minb2_unroll3"},
     {sweep_kernel<kLaplace, true, false, 4, 3, 2>, 4, "laplace_R4_minb3_unroll2"},
     {sweep_kernel<kLaplace, true, false, 1, 8, 2>, 1, "laplace_R1_minb8_unroll2"},
 };
 // energy sweeps (K1/K2 only, charges as targets), screened and kappa = 0
 static const SweepVariant kEnergyVariants[] = {
-    {sweep_kernel<kScreened, false, false, 6, 2, 2>, 6, "energy_R6_minb2_unroll2"},
+    {sweep_kernel<kScreened, false, false, 7, 2, 3>, 7, "energy_R7_minb2_unroll3"},
     {sweep_kernel<kScreened, false, false, 4, 3, 2>, 4, "energy_R4_minb3_unroll2"},
     {sweep_kernel<kScreened, false, false, 1, 8, 2>, 1, "energy_R1_minb8_unroll2"},
 };
 static const SweepVariant kEnergyLaplaceVariants[] = {
-    {sweep_kernel<kLaplace, false, false, 6, 2, 2>, 6, "energy_laplace_R6_minb2_unroll2"},
+    {sweep_kernel<kLaplace, false, false, 7, 2, 3>, 7, "energy_laplace_R7_minb2_unroll3"},
     {sweep_kernel<kLaplace, false, false, 4, 3, 2>, 4, "energy_laplace_R4_minb3_unroll2"},
     {sweep_kernel<kLaplace, false, false, 1, 8, 2>, 1, "energy_laplace_R1_minb8_unroll2"},
 };
 static const SweepVariant kLaplaceSelfVariants[] = {
-    {sweep_kernel<kLaplace, true, true, 6, 2, 2>, 6, "laplace_self_R6_minb2_unroll2"},
+    {sweep_kernel<kLaplace, true, true, 7, 2, 3>, 7, "laplace_self_R7_minb2_unroll3"},
     {sweep_kernel<kLaplace, true, true, 4, 3, 2>, 4, "laplace_self_R4_minb3_unroll2"},
     {sweep_kernel<kLaplace, true, true, 1, 6, 2>, 1, "laplace_self_R1_minb6_unroll2"},
 };
