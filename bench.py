@@ -4,6 +4,12 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
+--gpus N always means N GPUs (plan_launch): under torchrun WORLD_SIZE must
+equal N (one process per GPU, NCCL / fused peer-store gather); without a
+launcher and N > 1 one process drives N GPUs through the native group
+operator (csrc/hobi_group.cu).  Fewer than N visible GPUs, or a WORLD_SIZE
+other than N, exits with status 2 -- never a smaller run under an N label.
+
 A step is one application of the HOBI operator (SURVEY.md 8(a) rows a11-a14:
 source weights, all-pairs regular sweep, Duffy swap, diagonal, and for N > 1
 the gather of the row split: epilogue peer stores over NVLink once a start-up
@@ -19,8 +25,13 @@ quadrature point): N_v * 4 N_f = 1.342e10 pairs per step.
             inside every call), wall clock, max over ranks; `e2e.device_events`
             is the pinned host-buffer C-ABI step timed with CUDA events.
 `roofline`: the all-pairs sweep kernel, 96 canonical FP64 flops per pair
-             over its event-timed duration, against the FP64
-            DFMA peak measured in the same run (MEASURED_PEAKS.json has none).
+             over its event-timed duration (the slowest GPU's
+            for N > 1), against the FP64 DFMA peak measured on every GPU in
+            the same run (MEASURED_PEAKS.json has none); `traffic` is the
+            committed ncu capture only while its stamp matches the sweep
+            sources.
+`multi_gpu`: N > 1 only -- devices, row ranges, per-GPU compute and sweep ms,
+            exchange bytes per matvec and the step time not spent computing.
 `solve`   : one full GMRES solve of the config (restart 20, tol 1e-6) through
             the public API (wall clock, includes every matvec).
 `cpu_baseline`: the numpy restatement of the reference (oracle/, a "port";
@@ -74,7 +85,39 @@ def _dist():
     return rank, world, local
 
 
-def _workload(cfg, nv, nf, nq):
+class LaunchError(SystemExit):
+    """--gpus N cannot be honoured: exit non-zero with the reason, never a
+    silently smaller run."""
+
+    def __init__(self, msg):
+        super().__init__(2)
+        self.msg = msg
+
+
+def plan_launch(gpus: int, env, visible) -> str:
+    """How `--gpus N` runs: "torchrun" (one process per GPU, WORLD_SIZE from
+    the launcher, which must equal N), "group" (N > 1 without a launcher: one
+    process drives N GPUs through the native group operator) or "single".
+    `visible` is a callable returning the visible GPU count (asked only when
+    it matters).  Raises LaunchError when N cannot be honoured."""
+    if gpus < 1:
+        raise LaunchError(f"--gpus must be >= 1, got {gpus}")
+    if "WORLD_SIZE" in env:
+        world = int(env["WORLD_SIZE"])
+        if world != gpus:
+            raise LaunchError(f"--gpus {gpus} but the launcher started WORLD_SIZE={world} ranks")
+        return "torchrun" if world > 1 or env.get("HOBI_FORCE_NCCL") == "1" else "single"
+    if gpus == 1:
+        return "single"
+    n = visible()
+    if n < gpus:
+        raise LaunchError(f"--gpus {gpus} requested but only {n} GPU(s) are visible; "
+                          "refusing to report a smaller run under an N-GPU label")
+    return "group"
+
+
+def _workload(cfg, nv, nf, nq, n_gpus):
+    """`config` of the JSON line; identical for both arms at the same --gpus."""
     return {
         "workload": f"BASELINE config {cfg.name}: {nv} vertices, {nf} curved cubic triangles, "
                     f"{len(cfg.charges)} charges, eps {cfg.eps1:g}/{cfg.eps2:g}, kappa {cfg.kappa}",
@@ -82,6 +125,7 @@ def _workload(cfg, nv, nf, nq):
         "n_vertices": nv, "n_faces": nf, "quad_points_per_face": nq,
         "duffy_points": 16, "gmres_restart": cfg.restart, "gmres_tol": cfg.tol,
         "l2": "512 MiB scratch write between timed steps (inputs < L2)",
+        "parallelism": "single GPU" if n_gpus == 1 else f"row split over {n_gpus} GPUs (partition_targets)",
     }
 
 
@@ -93,7 +137,7 @@ class _Clocks:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, index):
+    def __init__(self, indices):
         self.samples, self.reasons, self.max_mhz = [], 0, None
         self._stop = threading.Event()
         try:
@@ -101,18 +145,22 @@ class _Clocks:
 
             pynvml.nvmlInit()
             self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            # CUDA ordinal -> NVML handle honouring CUDA_VISIBLE_DEVICES
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = [int(x) for x in vis.split(",")] if vis and all(x.strip().isdigit() for x in vis.split(",")) else None
+            self._h = [pynvml.nvmlDeviceGetHandleByIndex(phys[i] if phys else i) for i in indices]
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h[0], pynvml.NVML_CLOCK_SM)
         except Exception:  # noqa: BLE001
             self._nv = None
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
-                self.reasons |= self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-            except Exception:  # noqa: BLE001
-                pass
+            for h in self._h:
+                try:
+                    self.samples.append(self._nv.nvmlDeviceGetClockInfo(h, self._nv.NVML_CLOCK_SM))
+                    self.reasons |= self._nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:  # noqa: BLE001
+                    pass
             time.sleep(0.05)
 
     def __enter__(self):
@@ -189,7 +237,7 @@ def run_reference(a):
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _workload(cfg, nv, nf, nq), "impl": "reference",
+        "config": _workload(cfg, nv, nf, nq, a.gpus), "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": workers, "kind": "port",
                          "sample": f"{rows} target rows x {nsrc} sources per step (rows rotate), "
                                    f"oracle/hobi_oracle.py fork pool of {workers} workers"},
@@ -200,50 +248,27 @@ def run_reference(a):
     return 0
 
 
-def run_ours(a):
-    rank, world, local = _dist()
-    os.environ["HOBI_GATHER"] = a.gather
-    if world != a.gpus:
-        a.gpus = world
-    use_dist = world > 1 or ("RANK" in os.environ and os.environ.get("HOBI_FORCE_NCCL") == "1")
-    if use_dist:
-        import torch
-        import torch.distributed as dist
+class _RankRunner:
+    """One process per GPU (single GPU, or torchrun ranks over NCCL)."""
 
-        torch.cuda.set_device(local)
-        dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
-    os.environ.setdefault("HOBI_DEVICE", str(local))
-    from paper_1301_5914_b200 import (PhysicalParams, SolverConfig, assemble_rhs, discretize,
-                                      gmres_solve, make_operator, solvation_energy)
-    from paper_1301_5914_b200 import _native as N
-    from paper_1301_5914_b200.surfaces import baseline_config
-
-    lib = N.load()
-    cfg = baseline_config(a.config)
-    params = PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa)
-    scfg = SolverConfig(workers=1, restart=cfg.restart, tolerance=cfg.tol)
-    prob = discretize(cfg.mesh, params, cfg.charges, scfg)
-    h = prob.handle
-    nv, nf, nq = cfg.mesh.n_vertices, cfg.mesh.n_faces, 4
-    pairs_step = float(nv) * nf * nq
-    peak = C.c_double(0.0)
-    N.check(lib.hobi_probe_fp64_tflops(int(os.environ["HOBI_DEVICE"]), 300.0, C.byref(peak)))
-    u = np.random.default_rng(0).standard_normal(2 * nv)
-    out = np.empty_like(u)
-    lo, hi = (0, nv)
-    if world > 1:
+    def __init__(self, a, use_dist, lib, N, prob, world, rank):
+        self.a, self.use_dist, self.lib, self.N = a, use_dist, lib, N
+        self.prob, self.world, self.rank = prob, world, rank
+        self.handles = [prob.handle]
+        self.devices = [int(os.environ["HOBI_DEVICE"])]
+        nv = prob.n_collocation
         base, extra = divmod(nv, world)
         lo = rank * base + min(rank, extra)
-        hi = lo + base + (1 if rank < extra else 0)
+        self.ranges = [(lo, lo + base + (1 if rank < extra else 0))]
 
-    def barrier():
-        if use_dist:
+    def barrier(self):
+        if self.use_dist:
             import torch.distributed as dist
 
             dist.barrier()
 
-    def max_over_ranks(x):
-        if not use_dist:
+    def max_over_ranks(self, x):
+        if not self.use_dist:
             return x
         import torch
         import torch.distributed as dist
@@ -252,29 +277,153 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def gather_all(self, obj):
+        if not self.use_dist:
+            return [obj]
+        import torch.distributed as dist
+
+        box = [None] * self.world
+        dist.all_gather_object(box, obj)
+        return box
+
+    def bench(self, up, op, steps, mode, ms):
+        self.N.check(self.lib.hobi_bench(self.prob.handle, up, op, steps, mode, 1, self.N.dptr(ms)))
+
+    def op(self, make_operator, scfg):
+        return make_operator(self.prob, scfg)
+
+
+class _GroupRunner(_RankRunner):
+    """One process driving N GPUs through the native group operator."""
+
+    def __init__(self, a, lib, N, prob, op):
+        self.a, self.use_dist, self.lib, self.N = a, False, lib, N
+        self.prob, self.world, self.rank = prob, a.gpus, 0
+        self.group_op = op
+        pl = op.placement
+        if pl["mode"] != "group" or pl["workers"] != a.gpus or len(set(pl["devices"])) != a.gpus:
+            raise LaunchError(f"group operator did not place {a.gpus} GPUs: {pl}")
+        self.handles = op.member_handles
+        self.devices = pl["devices"]
+        n = a.gpus
+        lo, hi, direct = (C.c_int64 * n)(), (C.c_int64 * n)(), (C.c_int * n)()
+        N.check(lib.hobi_group_info(op.group, None, None, lo, hi, direct))
+        self.ranges = list(zip(lo, hi))
+        self.direct = list(direct)
+
+    def gather_all(self, obj):
+        return [obj]
+
+    def bench(self, up, op, steps, mode, ms):
+        self.N.check(self.lib.hobi_group_bench(self.group_op.group, up, op, steps, mode, 1, self.N.dptr(ms)))
+
+    def op(self, make_operator, scfg):
+        return self.group_op
+
+
+def _sweep_source_hash():
+    """SHA-256 of the sweep kernel's sources: stamps the committed ncu traffic."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in ("hobi_sweep.cu", "hobi_fastmath.cuh", "hobi_internal.cuh"):
+        with open(os.path.join(ROOT, "paper_1301_5914_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
+def _committed_traffic(config, world):
+    """ncu dram bytes of one sweep launch from profiles/sweep_traffic.json, only
+    if it was captured on this config/GPU count from the current sweep sources."""
+    tfile = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    try:
+        t = json.load(open(tfile))
+    except Exception:  # noqa: BLE001
+        return None, "no committed ncu capture"
+    if t.get("sweep_source_sha256") != _sweep_source_hash():
+        return None, "committed ncu capture is stale (sweep sources changed since)"
+    if t.get("config") != config or t.get("n_gpus", 1) != world:
+        return None, f"committed ncu capture is for config {t.get('config')} on {t.get('n_gpus', 1)} GPU(s)"
+    return t["bytes_per_launch"], t.get("source")
+
+
+def run_ours(a):
+    rank, world, local = _dist()
+    os.environ["HOBI_GATHER"] = a.gather
+    from paper_1301_5914_b200 import _native as N
+
+    mode = plan_launch(a.gpus, os.environ, N.device_count)
+    use_dist = mode == "torchrun"
+    if use_dist:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
+    if mode == "group":
+        os.environ["HOBI_DEVICE"] = "0"
+        local = 0
+    os.environ.setdefault("HOBI_DEVICE", str(local))
+    from paper_1301_5914_b200 import (PhysicalParams, SolverConfig, assemble_rhs, discretize,
+                                      gmres_solve, make_operator, solvation_energy)
+    from paper_1301_5914_b200.solver import GpuOperator
+    from paper_1301_5914_b200.surfaces import baseline_config
+
+    lib = N.load()
+    cfg = baseline_config(a.config)
+    params = PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa)
+    scfg = SolverConfig(workers=1, restart=cfg.restart, tolerance=cfg.tol)
+    prob = discretize(cfg.mesh, params, cfg.charges, scfg)
+    if mode == "group":
+        run = _GroupRunner(a, lib, N, prob, GpuOperator(prob, workers=a.gpus))
+        world = a.gpus
+    else:
+        run = _RankRunner(a, use_dist, lib, N, prob, world, rank)
+    nv, nf, nq = cfg.mesh.n_vertices, cfg.mesh.n_faces, 4
+    pairs_step = float(nv) * nf * nq
+    peaks = []
+    for d in run.devices:
+        pk = C.c_double(0.0)
+        N.check(lib.hobi_probe_fp64_tflops(d, 300.0, C.byref(pk)))
+        peaks.append(pk.value)
+    u = np.random.default_rng(0).standard_normal(2 * nv)
+    out = np.empty_like(u)
+    barrier, max_over_ranks = run.barrier, run.max_over_ranks
+
     # --- value: HBM-resident operator applications ---------------------------
-    ms = np.zeros(max(a.warmup, a.steps))
-    N.check(lib.hobi_bench(h, N.dptr(u), N.dptr(out), a.warmup, 0, 1, N.dptr(ms)))
+    ms = np.zeros(max(a.warmup, a.steps, 1))
+    run.bench(N.dptr(u), N.dptr(out), a.warmup, 0, ms)
     barrier()
-    N.check(lib.hobi_timing_reset(h))
-    with _Clocks(int(os.environ["HOBI_DEVICE"])) as clocks:
-        N.check(lib.hobi_bench(h, N.dptr(u), N.dptr(out), a.steps, 0, 1, N.dptr(ms)))
+    for h in run.handles:
+        N.check(lib.hobi_timing_reset(h))
+    with _Clocks(run.devices) as clocks:
+        run.bench(N.dptr(u), N.dptr(out), a.steps, 0, ms)
     barrier()
-    sweep_ms, sweep_n, launches = C.c_double(0), C.c_int64(0), C.c_int64(0)
-    N.check(lib.hobi_timing(h, C.byref(sweep_ms), C.byref(sweep_n), C.byref(launches)))
+    launches_total, members = 0, []
+    for h, (lo, hi) in zip(run.handles, run.ranges):
+        sweep_ms, sweep_n, launches = C.c_double(0), C.c_int64(0), C.c_int64(0)
+        N.check(lib.hobi_timing(h, C.byref(sweep_ms), C.byref(sweep_n), C.byref(launches)))
+        launches_total += int(launches.value)
+        members.append({"rows": [int(lo), int(hi)], "sweep_ms": sweep_ms.value / max(sweep_n.value, 1),
+                        "sweep_launches_per_step": sweep_n.value / max(a.steps, 1)})
     total_ms = max_over_ranks(float(ms[: a.steps].sum()))
     value = a.steps * pairs_step / (total_ms * 1e-3)
-    sweep_avg = sweep_ms.value / max(sweep_n.value, 1)
-    local_pairs = float(hi - lo) * nf * nq
-    achieved = local_pairs * FLOPS_PER_PAIR / (sweep_avg * 1e-3) * 1e-12
     ngroups, nspad = C.c_int(0), C.c_int64(0)
-    N.check(lib.hobi_sweep_layout(h, C.byref(ngroups), C.byref(nspad)))
+    N.check(lib.hobi_sweep_layout(prob.handle, C.byref(ngroups), C.byref(nspad)))
+    # per-GPU sweep: canonical flops of its rows over its own event-timed launches
+    for m in members:
+        lo, hi = m["rows"]
+        m["pairs"] = float(hi - lo) * nf * nq
+        m["achieved_tflops"] = m["pairs"] * FLOPS_PER_PAIR / (m["sweep_ms"] * 1e-3) * 1e-12 if m["sweep_ms"] else 0.0
+    all_members = [m for part in run.gather_all(members) for m in part]
+    worst = max(all_members, key=lambda m: m["sweep_ms"])
+    lo0, hi0 = members[0]["rows"]
     # per launch: source records (80 B) + this rank's targets (48 B) + the fixed
     # per-group partial sums (2 doubles per row per group) that keep row sums
     # independent of the split
-    algo_bytes = 80.0 * nspad.value + 48.0 * (hi - lo) + 16.0 * ngroups.value * (hi - lo)
+    algo_bytes = 80.0 * nspad.value + 48.0 * (hi0 - lo0) + 16.0 * ngroups.value * (hi0 - lo0)
 
-    # --- e2e: host buffers (pinned) through the C ABI, copies inside ------------
+    # --- e2e device events: host buffers (pinned) through the C ABI ------------
     try:
         import torch
 
@@ -285,10 +434,10 @@ def run_ours(a):
         pinned = True
     except Exception:  # noqa: BLE001
         up, op_, pinned = N.dptr(u), N.dptr(out), False
-    ms2 = np.zeros(max(a.warmup, a.steps))
-    N.check(lib.hobi_bench(h, up, op_, a.warmup, 1, 1, N.dptr(ms2)))
+    ms2 = np.zeros(max(a.warmup, a.steps, 1))
+    run.bench(up, op_, a.warmup, 1, ms2)
     barrier()
-    N.check(lib.hobi_bench(h, up, op_, a.steps, 1, 1, N.dptr(ms2)))
+    run.bench(up, op_, a.steps, 1, ms2)
     barrier()
     e2e_ms = max_over_ranks(float(ms2[: a.steps].sum()))
     e2e = a.steps * pairs_step / (e2e_ms * 1e-3)
@@ -296,30 +445,73 @@ def run_ours(a):
     # --- the call a user makes: the operator protocol on host numpy arrays
     # (solver.py:447-459), wall clock per synchronous call, L2 flushed between
     # calls outside the timed window -------------------------------------------
-    flush = None
+    flush = []
     try:
         import torch
 
-        flush = torch.empty(64 << 20, dtype=torch.float64, device=f"cuda:{os.environ['HOBI_DEVICE']}")
+        for d in run.devices:
+            flush.append(torch.empty(64 << 20, dtype=torch.float64, device=f"cuda:{d}"))
     except Exception:  # noqa: BLE001
-        flush = None
+        flush = []
     api_wall = []
     u_api, out_api = u, None
     if pinned:  # the step's input and result live in pinned host memory (views of hu / ho)
         u_api, out_api = hu.numpy(), ho.numpy()
-    with make_operator(prob, scfg) as op_api:
-        for _ in range(a.warmup):
-            op_api(u_api, out=out_api)
-        barrier()
-        for _ in range(a.steps):
-            if flush is not None:
-                flush.fill_(1.0)
-                torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            op_api(u_api, out=out_api)
-            api_wall.append(time.perf_counter() - t0)
+    op_api = run.op(make_operator, scfg)
+    for _ in range(a.warmup):
+        op_api(u_api, out=out_api)
+    barrier()
+    for _ in range(a.steps):
+        for f in flush:
+            f.fill_(1.0)
+        if flush:
+            for d in run.devices:
+                torch.cuda.synchronize(d)
+        t0 = time.perf_counter()
+        op_api(u_api, out=out_api)
+        api_wall.append(time.perf_counter() - t0)
+    if op_api is not getattr(run, "group_op", None):
+        op_api.close()
     api_ms = max_over_ranks(1e3 * float(sum(api_wall)))
     api = a.steps * pairs_step / (api_ms * 1e-3)
+
+    # --- multi-GPU exchange: per-GPU compute alone vs the whole step ----------
+    multi = None
+    if world > 1:
+        compute = []
+        for h, (lo, hi) in zip(run.handles, run.ranges):
+            msr = np.zeros(3)
+            N.check(lib.hobi_bench_rows(h, N.dptr(u), lo, hi, 3, 1, N.dptr(msr)))
+            compute.append(float(np.median(msr)))
+        slowest = max_over_ranks(max(compute))
+        step = total_ms / a.steps
+        if mode == "group":
+            xbytes = 16.0 * nv * (world - 1) + 16.0 * (nv - (run.ranges[0][1] - run.ranges[0][0]))
+            how = ("one process, one context per GPU (csrc/hobi_group.cu): iterate peer-copied "
+                   "to every member, each member's epilogue kernel stores its rows straight into "
+                   "device 0's output over NVLink peer memory"
+                   + ("" if all(run.direct) else " (some members staged: no peer access)"))
+            gather_mode = "group peer stores" if all(run.direct) else "group staged copies"
+        else:
+            p2p_on = C.c_int(0)
+            N.check(lib.hobi_comm_info(prob.handle, None, None, C.byref(p2p_on)))
+            xbytes = 16.0 * nv * (world - 1)
+            gather_mode = "fused epilogue + NVLink peer stores" if p2p_on.value else "ncclAllGather"
+            how = f"one process per GPU (torchrun), {gather_mode}, --gather {a.gather}"
+        ranks_info = run.gather_all({"device": run.devices, "rows": [list(r) for r in run.ranges],
+                                     "compute_ms": compute})
+        multi = {"mode": mode, "gather": gather_mode, "how": how,
+                 "devices": [d for r in ranks_info for d in r["device"]],
+                 "rows": [x for r in ranks_info for x in r["rows"]],
+                 "compute_ms_per_gpu": [x for r in ranks_info for x in r["compute_ms"]],
+                 "sweep_ms_per_gpu": [m["sweep_ms"] for m in all_members],
+                 "step_ms": step,
+                 "exchange_ms": max(step - slowest, 0.0),
+                 "exchange_bytes_per_matvec": xbytes,
+                 "exchange_GBps": xbytes / max(step - slowest, 1e-6) * 1e-6,
+                 "note": "exchange_ms = device step time minus the slowest GPU's compute-only "
+                         "time for its rows (hobi_bench_rows); it includes the stream/event "
+                         "synchronisation, not only bytes in flight"}
 
     # --- solve through the public API ------------------------------------------
     solve = None
@@ -327,8 +519,10 @@ def run_ours(a):
         barrier()
         t0 = time.perf_counter()
         b = assemble_rhs(prob)
-        with make_operator(prob, scfg) as op:
-            sol = gmres_solve(op, b, scfg)
+        op = run.op(make_operator, scfg)
+        sol = gmres_solve(op, b, scfg)
+        if op is not getattr(run, "group_op", None):
+            op.close()
         energy = solvation_energy(prob, sol)
         barrier()
         dt = max_over_ranks(time.perf_counter() - t0)
@@ -338,22 +532,23 @@ def run_ours(a):
 
     # one-GPU model of the p-way row split: the slowest of the first and last
     # rank's compute (everything before the gather), device-timed; labelled a
-    # model -- the real multi-GPU numbers come from torchrun runs of this file
+    # model -- measured multi-GPU numbers come from --gpus N runs of this file
     split_model = None
     if world == 1:
-        split_model = {"what": "slowest-rank compute of a p-way split timed on this GPU (no collective)"}
+        split_model = {"what": "MODEL, not a multi-GPU run: slowest-rank compute of a p-way split "
+                               "timed on this one GPU (no collective)"}
         t1 = None
         for p in (1, 2, 4, 8):
-            worst = 0.0
+            worst_ms = 0.0
             for r in ((0,) if p == 1 else (0, p - 1)):
                 base, extra = divmod(nv, p)
                 rlo = r * base + min(r, extra)
                 rhi = rlo + base + (1 if r < extra else 0)
                 msr = np.zeros(3)
-                N.check(lib.hobi_bench_rows(h, N.dptr(u), rlo, rhi, 3, 1, N.dptr(msr)))
-                worst = max(worst, float(np.median(msr)))
-            t1 = worst if p == 1 else t1
-            split_model[str(p)] = {"rank_ms": worst, "efficiency": t1 / (p * worst)}
+                N.check(lib.hobi_bench_rows(prob.handle, N.dptr(u), rlo, rhi, 3, 1, N.dptr(msr)))
+                worst_ms = max(worst_ms, float(np.median(msr)))
+            t1 = worst_ms if p == 1 else t1
+            split_model[str(p)] = {"rank_ms": worst_ms, "efficiency": t1 / (p * worst_ms)}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -370,62 +565,60 @@ def run_ours(a):
         if solve:
             cpu["extrapolated"]["solve_s"] = solve["matvecs"] * pairs_step / rate
 
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "sweep_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            t = json.load(open(tfile))
-            if t.get("config") == a.config and t.get("n_gpus", 1) == world:
-                traffic = t["bytes_per_launch"]
-        except Exception:  # noqa: BLE001
-            traffic = None
+    traffic, traffic_src = _committed_traffic(a.config, world)
     # executed-instruction view of the same launches: FP64 lane-ops per clock
     # per SM against the pipe's 64 (the canonical-flop frac above is the headline)
     clk = clocks.summary()
     pipe = None
     sms = C.c_int(0)
-    if clk.get("sm_mhz") and lib.hobi_device_sms(int(os.environ["HOBI_DEVICE"]), C.byref(sms)) == 0:
-        ops = FP64_INSTR_PER_PAIR * local_pairs / (sweep_avg * 1e-3) / (sms.value * clk["sm_mhz"] * 1e6)
+    if clk.get("sm_mhz") and lib.hobi_device_sms(run.devices[0], C.byref(sms)) == 0:
+        m0 = members[0]
+        ops = FP64_INSTR_PER_PAIR * m0["pairs"] / (m0["sweep_ms"] * 1e-3) / (sms.value * clk["sm_mhz"] * 1e6)
         pipe = {"instr_per_pair": FP64_INSTR_PER_PAIR, "lane_ops_per_clk_per_sm": ops,
-                "frac_of_64": ops / 64.0, "sms": sms.value, "sm_mhz": clk["sm_mhz"]}
+                "frac_of_64": ops / 64.0, "sms": sms.value, "sm_mhz": clk["sm_mhz"], "gpu": run.devices[0]}
+    peak_all = run.gather_all(peaks)
+    peak_total = float(sum(p for part in peak_all for p in part))
+    # whole-job sweep rate: every GPU's pairs over the slowest GPU's sweep time
+    achieved = pairs_step * FLOPS_PER_PAIR / (worst["sweep_ms"] * 1e-3) * 1e-12
+    launches_total = int(max_over_ranks(float(launches_total)))
     if rank == 0:
-        conf = _workload(cfg, nv, nf, nq)
-        p2p_on = C.c_int(0)
-        N.check(lib.hobi_comm_info(h, None, None, C.byref(p2p_on)))
-        conf["parallelism"] = (f"row split x{world} + " + ("fused epilogue/NVLink peer-store gather"
-                                                            if p2p_on.value else "NCCL allgather")
-                               + f" (--gather {a.gather})") if world > 1 else "single GPU"
         line = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": conf,
-            "e2e": {"value": api, "unit": "pairs/s", "h2d_bytes_per_step": 16 * nv * world,
-                    "d2h_bytes_per_step": 16 * nv * world, "ms_per_step": api_ms / a.steps,
+            "config": _workload(cfg, nv, nf, nq, world),
+            "e2e": {"value": api, "unit": "pairs/s", "h2d_bytes_per_step": 16 * nv * (1 if mode == "group" else world),
+                    "d2h_bytes_per_step": 16 * nv * (1 if mode == "group" else world),
+                    "ms_per_step": api_ms / a.steps,
                     "pinned": pinned,
                     "how": "wall clock of the public operator call op(u, out=...) on host arrays "
                            "(make_operator, solver.py:447-459), "
                            + ("pinned " if pinned else "pageable ")
                            + "H2D + matvec + D2H inside each call, max over ranks; L2 flushed between "
-                           "calls" + ("" if flush is not None else " (flush unavailable)"),
+                           "calls" + ("" if flush else " (flush unavailable)"),
                     "device_events": {"value": e2e, "ms_per_step": e2e_ms / a.steps, "pinned": pinned,
-                                      "how": "hobi_bench mode 1: pinned H2D + matvec + D2H between "
-                                             "CUDA events on the library stream"}},
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                         "frac": achieved / peak.value, "traffic": traffic,
+                                      "how": "bench mode 1: pinned H2D + matvec + D2H between "
+                                             "CUDA events on the (leader's) library stream"}},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_total, "unit": "TFLOP/s",
+                         "frac": achieved / peak_total, "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes": algo_bytes,
                          "kernel": "sweep_kernel<kScreened,FULL>", "flops_per_pair": FLOPS_PER_PAIR,
-                         "avg_launch_ms": sweep_avg, "pairs_per_launch": local_pairs,
-                         "peak_source": "DFMA probe in this run (hobi_probe_fp64_tflops); "
-                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "avg_launch_ms": worst["sweep_ms"], "pairs_per_launch": worst["pairs"],
+                         "per_gpu": [{"rows": m["rows"], "sweep_ms": m["sweep_ms"],
+                                      "achieved_tflops": m["achieved_tflops"]} for m in all_members],
+                         "peak_source": "DFMA probe on each GPU in this run (hobi_probe_fp64_tflops), "
+                                        "summed over GPUs; MEASURED_PEAKS.json has no FP64 entry",
                          "fp64_pipe": pipe},
-            "gpu_launches": int(launches.value),
+            "gpu_launches": launches_total,
             "clocks": clk,
             "solve": solve,
+            "multi_gpu": multi,
             "split_model": split_model,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if mode == "group":
+        run.group_op.close()
     prob.close()  # release the device context and its NCCL communicator before torch's
     if use_dist:
         import torch.distributed as dist
@@ -438,7 +631,11 @@ def main():
     a = _args()
     if a.impl == "reference":
         return run_reference(a)
-    return run_ours(a)
+    try:
+        return run_ours(a)
+    except LaunchError as exc:
+        print(f"bench.py: {exc.msg}", file=sys.stderr, flush=True)
+        return 2
 
 
 if __name__ == "__main__":

@@ -198,6 +198,25 @@ int hobi_comm_p2p_open(hobi_ctx* ctx, const unsigned char* handles, int nranks, 
 /* Fall back from the peer-store gather to the communicator's ncclAllGather
  * (permanently, e.g. when a start-up check of the P2P path fails). */
 int hobi_comm_p2p_disable(hobi_ctx* ctx);
+/*
+ * P2P-only row split (no NCCL communicator): this context owns rows
+ * partition_targets(n, nranks)[rank]; follow with hobi_comm_p2p_handle /
+ * hobi_comm_p2p_open.  For ranks that have no NCCL (or share a device, where
+ * NCCL refuses two ranks).  Until the peers are open a matvec fails with
+ * HOBI_ERR_STATE; RHS and energy run unsplit (bitwise the same values).
+ */
+int hobi_comm_init_p2p(hobi_ctx* ctx, int nranks, int rank);
+/*
+ * One P2P-gathered operator application in two host-ordered halves, for
+ * ranks whose kernels must not wait on one another (several ranks on one
+ * time-sliced GPU): phase 0 copies u in, computes this rank's rows and stores
+ * them into every rank's receive area (arrival counters bumped), then
+ * synchronises; phase 1 -- called once every rank has finished phase 0 (a
+ * host barrier) -- finds every arrival in place, copies the gathered A u out
+ * and checks the watchdog.  hobi_matvec == phase 0 + phase 1 without the
+ * host round trip.  Phases must alternate (HOBI_ERR_STATE otherwise).
+ */
+int hobi_matvec_p2p_phase(hobi_ctx* ctx, const double* u, double* out, int phase);
 /* Row-split state: ranks, this rank, and whether the P2P gather is active. */
 int hobi_comm_info(hobi_ctx* ctx, int* nranks, int* rank, int* p2p);
 
@@ -221,6 +240,15 @@ int hobi_group_destroy(hobi_group* group);
 int hobi_group_matvec(hobi_group* group, const double* u, double* out);
 int hobi_group_gmres(hobi_group* group, const double* b, double tol, int restart, int max_it, double* x,
                      int* iterations, double* residual, double* best, int* matvecs);
+/* Placement of a group: member count, and per member (arrays of `size`, any
+ * may be NULL) its device, row range [lo, hi) and whether its epilogue stores
+ * straight into the leader's output (1) or stages a copy (0). */
+int hobi_group_info(hobi_group* group, int* size, int* devices, int64_t* lo, int64_t* hi, int* direct);
+/* hobi_bench for a group: each step bracketed by CUDA events on the leader's
+ * stream, which waits for every member, so ms[i] is the slowest device's
+ * time; flush_l2 flushes every member's L2 between steps. */
+int hobi_group_bench(hobi_group* group, const double* u, double* out, int steps, int mode, int flush_l2,
+                     double* ms);
 /* Single-GPU emulation of an nranks-way split (same buffers, same gather
  * layout and permutation kernel, no NCCL): for determinism tests. */
 int hobi_emulate_ranks(hobi_ctx* ctx, int nranks);

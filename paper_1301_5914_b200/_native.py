@@ -65,6 +65,9 @@ SIGNATURES = {
     "hobi_group_matvec": (C.c_int, [C.c_void_p, _dp, _dp]),
     "hobi_group_gmres": (C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, C.c_int, _dp, C.POINTER(C.c_int),
                                    _dp, _dp, C.POINTER(C.c_int)]),
+    "hobi_group_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _i64p, _i64p,
+                                  C.POINTER(C.c_int)]),
+    "hobi_group_bench": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp]),
     "hobi_export_caches": (C.c_int, [_ctxp, _dp, _dp, _dp, _dp, _dp, _dp, _i64p, _i64p, _i64p, _i64p]),
     "hobi_export_nodes": (C.c_int, [_ctxp, _dp, _dp]),
     "hobi_kernel_values": (C.c_int, [C.c_int, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_double,
@@ -74,6 +77,8 @@ SIGNATURES = {
     "hobi_emulate_ranks": (C.c_int, [_ctxp, C.c_int]),
     "hobi_comm_p2p_handle": (C.c_int, [_ctxp, C.POINTER(C.c_ubyte)]),
     "hobi_comm_p2p_open": (C.c_int, [_ctxp, C.POINTER(C.c_ubyte), C.c_int, C.c_int]),
+    "hobi_comm_init_p2p": (C.c_int, [_ctxp, C.c_int, C.c_int]),
+    "hobi_matvec_p2p_phase": (C.c_int, [_ctxp, _dp, _dp, C.c_int]),
     "hobi_timing_reset": (C.c_int, [_ctxp]),
     "hobi_timing": (C.c_int, [_ctxp, _dp, _i64p, _i64p]),
     "hobi_pairs_per_matvec": (C.c_int, [_ctxp, _dp]),
@@ -94,17 +99,30 @@ class NativeError(RuntimeError):
 
 
 def load():
-    """Load libhobi.so (building it first if the sources are newer)."""
+    """Load libhobi.so, building it first when it is missing or older than its
+    sources (build._stale).  Concurrent first loads (every torchrun rank) are
+    serialised by an exclusive lock on a file next to the library, so exactly
+    one process builds and the others load its result."""
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        try:
-            from . import build as _build
+    from . import build as _build
 
-            _build.build()
+    if _build.sources_present() and _build._stale():
+        import fcntl
+
+        try:
+            with open(os.path.join(_HERE, ".build.lock"), "w") as lock:
+                fcntl.flock(lock, fcntl.LOCK_EX)
+                if _build._stale():
+                    _build.build()
         except Exception as exc:  # noqa: BLE001
-            raise ImportError(f"libhobi.so is missing and could not be built: {exc}") from exc
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"libhobi.so is missing and could not be built: {exc}") from exc
+            import warnings
+
+            warnings.warn(f"libhobi.so is older than its sources and the rebuild failed ({exc}); "
+                          "loading the existing library", RuntimeWarning, stacklevel=2)
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)

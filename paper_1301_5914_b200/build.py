@@ -40,21 +40,48 @@ def _nvcc():
     raise RuntimeError("nvcc not found")
 
 
-def _stale():
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+def _deps():
     deps = [os.path.join(CSRC, f) for f in list(UNITS) + HEADERS]
     deps.append(os.path.join(ROOT, "include", "hobi.h"))
     deps.append(os.path.abspath(__file__))
-    return any(os.path.getmtime(d) > t for d in deps)
+    return deps
+
+
+def source_hash() -> str:
+    """SHA-256 over the library's sources and this recipe (content, not
+    mtimes: a repo snapshot copied to another machine keeps its built library)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for d in _deps():
+        with open(d, "rb") as f:
+            h.update(os.path.basename(d).encode() + b"\0" + f.read())
+    return h.hexdigest()
+
+
+STAMP = LIB + ".srchash"
+
+
+def _stale():
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    with open(STAMP) as f:
+        return f.read().strip() != source_hash()
+
+
+def sources_present() -> bool:
+    """False on a box that received only the built library."""
+    return all(os.path.exists(os.path.join(CSRC, f)) for f in UNITS)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     nvcc = _nvcc()
-    objdir = os.path.join(HERE, "_build")
+    stamp = source_hash()  # of the sources this build compiles
+    # objects and the temporary library are private to this process, so two
+    # builders can never interleave writes into one file
+    objdir = os.path.join(HERE, "_build", f"p{os.getpid()}")
     os.makedirs(objdir, exist_ok=True)
     objs, cmds = [], []
     for unit, extra in UNITS.items():
@@ -71,9 +98,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as pool:
         for res in pool.map(lambda c: subprocess.run(c, check=True), cmds):
             del res
-    tmp = LIB + ".tmp"
+    tmp = f"{LIB}.{os.getpid()}.tmp"
     subprocess.run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"], check=True)
     os.replace(tmp, LIB)
+    with open(STAMP + ".tmp", "w") as f:
+        f.write(stamp + "\n")
+    os.replace(STAMP + ".tmp", STAMP)
+    import shutil
+
+    shutil.rmtree(objdir, ignore_errors=True)
     return LIB
 
 

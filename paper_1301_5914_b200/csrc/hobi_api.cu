@@ -107,7 +107,10 @@ static int setup_gather(hobi_ctx* c, int nranks) {
   c->gather_m = (c->nt + nranks - 1) / nranks;
   if (c->gather_send.alloc(2 * c->gather_m) || c->gather_recv.alloc((size_t)nranks * 2 * c->gather_m))
     return HOBI_ERR_CUDA;
-  HOBI_CUDA(cudaMemset(c->gather_recv.p, 0, (size_t)nranks * 2 * c->gather_m * sizeof(double)));
+  // on the context stream (non-blocking, so not ordered after the legacy
+  // stream), finished before any later work can touch the buffer
+  HOBI_CUDA(cudaMemsetAsync(c->gather_recv.p, 0, (size_t)nranks * 2 * c->gather_m * sizeof(double), c->stream));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
 }
 
@@ -250,6 +253,18 @@ int hobi_device_sms(int device, int* sms) {
   return 0;
 }
 
+// Mesh-size and face-index checks shared by every constructor: sizes must fit
+// the device's int32 indices, and every face must reference vertices in [0, nv).
+static int check_faces(const int64_t* faces, int64_t nv, int64_t nf) {
+  if (nv < 1 || nf < 1) return fail(HOBI_ERR_VALUE, "mesh must have vertices and faces");
+  if (nv >= (1ll << 31) || 3 * nf >= (1ll << 31)) return fail(HOBI_ERR_VALUE, "mesh too large");
+  for (int64_t i = 0; i < 3 * nf; ++i)
+    if (faces[i] < 0 || faces[i] >= nv)
+      return fail(HOBI_ERR_VALUE, "face " + std::to_string(i / 3) + " references a vertex outside [0, " +
+                                      std::to_string(nv) + ")");
+  return 0;
+}
+
 int hobi_create(int device, const double* vertices, const double* normals, int64_t nv,
                 const int64_t* faces, int64_t nf, double eps1, double eps2, double kappa,
                 const double* reg_pts, const double* reg_wts, const double* reg_shape, int nq,
@@ -259,15 +274,10 @@ int hobi_create(int device, const double* vertices, const double* normals, int64
   *out = nullptr;
   if (nq < 1 || nq > 16) return fail(HOBI_ERR_VALUE, "regular rule must have 1..16 points");
   if (nd < 1 || nd > 64) return fail(HOBI_ERR_VALUE, "Duffy rule must have 1..64 points");
-  if (nv < 1 || nf < 1) return fail(HOBI_ERR_VALUE, "mesh must have vertices and faces");
-  if (nv >= (1ll << 31) || 3 * nf >= (1ll << 31)) return fail(HOBI_ERR_VALUE, "mesh too large");
-  for (int64_t i = 0; i < 3 * nf; ++i)
-    if (faces[i] < 0 || faces[i] >= nv)
-      return fail(HOBI_ERR_VALUE, "face " + std::to_string(i / 3) + " references a vertex outside [0, " +
-                                      std::to_string(nv) + ")");
+  int rc;
+  if ((rc = check_faces(faces, nv, nf))) return rc;
   InitTrace tr;
   hobi_ctx* c = new hobi_ctx();
-  int rc;
   auto bail = [&](int r) {
     hobi_destroy(c);
     return r;
@@ -384,19 +394,29 @@ int hobi_create_from_caches(int device, const double* vertices, const double* no
                             const int64_t* pair_gverts, const int64_t* pair_starts, hobi_ctx** out) {
   *out = nullptr;
   if (nq < 1 || nq > 16 || nd < 1 || nd > 64) return fail(HOBI_ERR_VALUE, "rule sizes out of range");
-  if (nv < 1 || nf < 1) return fail(HOBI_ERR_VALUE, "mesh must have vertices and faces");
-  if (nv >= (1ll << 31) || 3 * nf >= (1ll << 31)) return fail(HOBI_ERR_VALUE, "mesh too large");
+  int rc;
+  if ((rc = check_faces(faces, nv, nf))) return rc;
   const int64_t np = 3 * nf;
+  // the pair tables index device arrays in the Duffy swap and the epilogue:
+  // a CSR over vertices, pairs in range, each pair's vertex inside its segment
   if (pair_starts[0] != 0 || pair_starts[nv] != np)
     return fail(HOBI_ERR_VALUE, "pair_starts must run from 0 to 3*n_faces");
-  for (int64_t i = 0; i < 3 * nf; ++i)
-    if (faces[i] < 0 || faces[i] >= nv) return fail(HOBI_ERR_VALUE, "face index out of range");
+  for (int64_t v = 0; v < nv; ++v) {
+    if (pair_starts[v + 1] < pair_starts[v]) return fail(HOBI_ERR_VALUE, "pair_starts must be non-decreasing");
+    for (int64_t p = pair_starts[v]; p < pair_starts[v + 1]; ++p)
+      if (pair_vertex[p] != v) return fail(HOBI_ERR_VALUE, "pair_vertex disagrees with pair_starts");
+  }
+  for (int64_t p = 0; p < np; ++p) {
+    if (pair_face[p] < 0 || pair_face[p] >= nf) return fail(HOBI_ERR_VALUE, "pair_face out of range");
+    for (int k = 0; k < 3; ++k)
+      if (pair_gverts[3 * p + k] < 0 || pair_gverts[3 * p + k] >= nv)
+        return fail(HOBI_ERR_VALUE, "pair_gverts out of range");
+  }
   hobi_ctx* c = new hobi_ctx();
   auto bail = [&](int r) {
     hobi_destroy(c);
     return r;
   };
-  int rc;
   if ((rc = common_init(c, device, eps1, eps2, kappa))) return bail(rc);
   if ((rc = check_extent(c, vertices, nv))) return bail(rc);
   c->scheme = kHobi;
@@ -454,13 +474,13 @@ int hobi_create_lobi(int device, const double* vertices, const double* normals, 
                      hobi_ctx** out) {
   (void)normals;
   *out = nullptr;
-  if (nv < 1 || nf < 1) return fail(HOBI_ERR_VALUE, "mesh must have vertices and faces");
+  int rc;
+  if ((rc = check_faces(faces, nv, nf))) return rc;
   hobi_ctx* c = new hobi_ctx();
   auto bail = [&](int r) {
     hobi_destroy(c);
     return r;
   };
-  int rc;
   if ((rc = common_init(c, device, eps1, eps2, kappa))) return bail(rc);
   if ((rc = check_extent(c, vertices, nv))) return bail(rc);
   c->scheme = kLobi;
@@ -746,14 +766,33 @@ int hobi_comm_init(hobi_ctx* c, const unsigned char id[128], int nranks, int ran
   return setup_gather(c, nranks);
 }
 
+int hobi_comm_init_p2p(hobi_ctx* c, int nranks, int rank) {
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(HOBI_ERR_VALUE, "bad rank/nranks");
+  if (nranks > kMaxRanks) return fail(HOBI_ERR_VALUE, "P2P gather supports at most 64 ranks");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->comm.nccl && nccl::api().loaded) nccl::api().destroy(c->comm.nccl);
+  c->comm = Comm();
+  c->comm.nranks = nranks;
+  c->comm.rank = rank;
+  c->comm.p2p_only = true;
+  row_range(c->nt, nranks, rank, &c->lo, &c->hi);
+  return 0;
+}
+
 int hobi_comm_p2p_handle(hobi_ctx* c, unsigned char handle[64]) {
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   HOBI_CUDA(cudaSetDevice(c->device));
   // two (2 nt) receive buffers + arrival counters [parity][source rank]
   if (c->comm.nranks > kMaxRanks) return fail(HOBI_ERR_VALUE, "P2P gather supports at most 64 ranks");
+  if (c->comm.p2p) return fail(HOBI_ERR_STATE, "the P2P gather is active: its area cannot be re-exported");
   const size_t n = 4 * (size_t)c->nt + 2 * kMaxRanks;
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
   if (c->p2p_area.alloc(n)) return HOBI_ERR_CUDA;
-  HOBI_CUDA(cudaMemset(c->p2p_area.p, 0, n * sizeof(double)));
+  HOBI_CUDA(cudaMemsetAsync(c->p2p_area.p, 0, n * sizeof(double), c->stream));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  c->comm.p2p_fresh = true;
   cudaIpcMemHandle_t h;
   HOBI_CUDA(cudaIpcGetMemHandle(&h, c->p2p_area.p));
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
@@ -764,6 +803,11 @@ int hobi_comm_p2p_handle(hobi_ctx* c, unsigned char handle[64]) {
 int hobi_comm_p2p_open(hobi_ctx* c, const unsigned char* handles, int nranks, int rank) {
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   if (!c->p2p_area.p) return fail(HOBI_ERR_STATE, "hobi_comm_p2p_handle must be called first");
+  // the arrival counters count from zero: an area that was opened before (even
+  // if the gather was disabled since) needs a fresh hobi_comm_p2p_handle and a
+  // new exchange, or stale counts would release rows before they arrive
+  if (!c->comm.p2p_fresh)
+    return fail(HOBI_ERR_STATE, "P2P receive area already used: call hobi_comm_p2p_handle again first");
   if (nranks != c->comm.nranks || rank != c->comm.rank)
     return fail(HOBI_ERR_STATE, "P2P ranks differ from the communicator (call hobi_comm_init first)");
   HOBI_CUDA(cudaSetDevice(c->device));
@@ -781,8 +825,10 @@ int hobi_comm_p2p_open(hobi_ctx* c, const unsigned char* handles, int nranks, in
     ptrs[r] = static_cast<double*>(p);
   }
   if (c->p2p_peers.alloc(nranks) || c->p2p_done.alloc(1)) return HOBI_ERR_CUDA;
-  HOBI_CUDA(cudaMemcpy(c->p2p_peers.p, ptrs.data(), nranks * sizeof(double*), cudaMemcpyHostToDevice));
-  HOBI_CUDA(cudaMemset(c->p2p_done.p, 0, sizeof(unsigned)));
+  HOBI_CUDA(cudaMemcpyAsync(c->p2p_peers.p, ptrs.data(), nranks * sizeof(double*), cudaMemcpyHostToDevice,
+                            c->stream));
+  HOBI_CUDA(cudaMemsetAsync(c->p2p_done.p, 0, sizeof(unsigned), c->stream));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
   if (!c->p2p_err) {
     HOBI_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->p2p_err), sizeof(int), cudaHostAllocMapped));
     HOBI_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->p2p_err_dev), c->p2p_err, 0));
@@ -794,8 +840,35 @@ int hobi_comm_p2p_open(hobi_ctx* c, const unsigned char* handles, int nranks, in
   const char* extra = getenv("HOBI_P2P_TEST_MISSING_ARRIVALS");
   c->p2p_extra = extra ? (unsigned long long)atoll(extra) : 0;
   c->comm.p2p = true;
+  c->comm.p2p_fresh = false;
+  c->comm.p2p_pending = false;
   c->comm.epoch = 0;
   return 0;
+}
+
+int hobi_matvec_p2p_phase(hobi_ctx* c, const double* u, double* out, int phase) {
+  NvtxRange nvtx_("hobi_matvec_p2p_phase");
+  if (!c) return fail(HOBI_ERR_STATE, "null context");
+  if (!c->comm.p2p) return fail(HOBI_ERR_STATE, "the P2P gather is not active");
+  if (phase != 0 && phase != 1) return fail(HOBI_ERR_VALUE, "phase must be 0 (send) or 1 (receive)");
+  if ((phase == 0) == c->comm.p2p_pending)
+    return fail(HOBI_ERR_STATE, phase == 0 ? "the previous send phase has no receive phase yet"
+                                           : "no send phase is pending");
+  HOBI_CUDA(cudaSetDevice(c->device));
+  const size_t bytes = 2 * c->nt * sizeof(double);
+  int rc;
+  if (phase == 0) {
+    HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, bytes, cudaMemcpyHostToDevice, c->stream));
+    if ((rc = matvec_p2p_send(c, c->u.p))) return rc;
+    HOBI_CUDA(cudaStreamSynchronize(c->stream));  // rows and arrival counts are out
+    c->comm.p2p_pending = true;
+    return 0;
+  }
+  c->comm.p2p_pending = false;
+  if ((rc = matvec_p2p_recv(c, c->out.p))) return rc;
+  HOBI_CUDA(cudaMemcpyAsync(out, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  return p2p_check(c);
 }
 
 int hobi_comm_p2p_disable(hobi_ctx* c) {
@@ -803,6 +876,7 @@ int hobi_comm_p2p_disable(hobi_ctx* c) {
   HOBI_CUDA(cudaSetDevice(c->device));
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
   c->comm.p2p = false;  // the NCCL gather (set up by hobi_comm_init) takes over
+  c->comm.p2p_pending = false;
   return 0;
 }
 

@@ -200,6 +200,112 @@ int hobi_group_matvec(hobi_group* g, const double* u, double* out) {
   return 0;
 }
 
+int hobi_group_info(hobi_group* g, int* size, int* devices, int64_t* lo, int64_t* hi, int* direct) {
+  if (!g) return fail(HOBI_ERR_STATE, "null group");
+  if (size) *size = (int)g->m.size();
+  for (size_t i = 0; i < g->m.size(); ++i) {
+    if (devices) devices[i] = g->m[i].device;
+    if (lo) lo[i] = g->m[i].lo;
+    if (hi) hi[i] = g->m[i].hi;
+    if (direct) direct[i] = g->m[i].direct ? 1 : 0;
+  }
+  return 0;
+}
+
+// Timed group applications, the group analogue of hobi_bench: each step is
+// bracketed by CUDA events on the leader's stream, and the leader's stream
+// waits for every member's finishing event before the closing event, so a
+// step's time is the slowest device's (max over the group).  Every member's
+// L2 is flushed before the step (outside the brackets) when flush_l2 != 0.
+int hobi_group_bench(hobi_group* g, const double* u, double* out, int steps, int mode, int flush_l2,
+                     double* ms) {
+  if (!g) return fail(HOBI_ERR_STATE, "null group");
+  if (steps < 0 || (mode != 0 && mode != 1)) return fail(HOBI_ERR_VALUE, "bad bench arguments");
+  hobi_ctx* lead = g->m[0].c;
+  const size_t bytes = 2 * g->nt * sizeof(double);
+  const size_t flush_bytes = (size_t)512 << 20;
+  const size_t n = g->m.size();
+  std::vector<DevBuf<unsigned char>> scratch(n);
+  std::vector<cudaEvent_t> flushed(n, nullptr);
+  auto cleanup = [&]() {
+    for (size_t i = 0; i < n; ++i) {
+      cudaSetDevice(g->m[i].device);
+      if (flushed[i]) cudaEventDestroy(flushed[i]);
+      scratch[i].release();
+    }
+    cudaSetDevice(lead->device);
+  };
+  int rc = 0;
+  for (size_t i = 0; i < n && !rc; ++i) {
+    if (cudaSetDevice(g->m[i].device) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "cudaSetDevice");
+    if (!rc && flush_l2) rc = scratch[i].alloc(flush_bytes);
+    if (!rc) {
+      cudaError_t e = cudaEventCreateWithFlags(&flushed[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) rc = cuda_fail(e, "cudaEventCreate");
+    }
+  }
+  if (rc) {
+    cleanup();
+    return rc;
+  }
+  EventPair ev;
+  cudaSetDevice(lead->device);
+  cudaError_t e = ev.create();
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "cudaEventCreate");
+  }
+  GroupOperator op(g);
+  if (mode == 0) {
+    e = cudaMemcpyAsync(lead->u.p, u, bytes, cudaMemcpyHostToDevice, lead->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync");
+  }
+  for (int s = 0; s < steps && !rc; ++s) {
+    for (size_t i = 0; i < n && !rc; ++i) {  // flush every member's L2, outside the brackets
+      Member& mb = g->m[i];
+      cudaSetDevice(mb.device);
+      if (flush_l2) e = cudaMemsetAsync(scratch[i].p, s & 0xff, flush_bytes, mb.c->stream);
+      if (e == cudaSuccess) e = cudaEventRecord(flushed[i], mb.c->stream);
+      if (e != cudaSuccess) rc = cuda_fail(e, "flush");
+    }
+    if (rc) break;
+    cudaSetDevice(lead->device);
+    for (size_t i = 0; i < n; ++i) cudaStreamWaitEvent(lead->stream, flushed[i], 0);
+    e = cudaEventRecord(ev.a, lead->stream);
+    if (e == cudaSuccess && mode == 1)
+      e = cudaMemcpyAsync(lead->u.p, u, bytes, cudaMemcpyHostToDevice, lead->stream);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "bench step");
+      break;
+    }
+    rc = op.apply(lead->u.p, lead->out.p);  // ends with the leader waiting on every member
+    if (rc) break;
+    cudaSetDevice(lead->device);
+    if (mode == 1) e = cudaMemcpyAsync(out, lead->out.p, bytes, cudaMemcpyDeviceToHost, lead->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ev.b, lead->stream);
+    if (e == cudaSuccess) e = cudaEventSynchronize(ev.b);
+    float t = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, ev.a, ev.b);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "bench step");
+      break;
+    }
+    ms[s] = t;
+  }
+  if (!rc && mode == 0 && out) {
+    cudaSetDevice(lead->device);
+    e = cudaMemcpyAsync(out, lead->out.p, bytes, cudaMemcpyDeviceToHost, lead->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(lead->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "bench readback");
+  }
+  for (size_t i = 0; i < n; ++i) {  // the scratch buffers must not be freed under a pending memset
+    cudaSetDevice(g->m[i].device);
+    cudaStreamSynchronize(g->m[i].c->stream);
+  }
+  cleanup();
+  return rc;
+}
+
 int hobi_group_gmres(hobi_group* g, const double* b, double tol, int restart, int max_it, double* x,
                      int* iterations, double* residual, double* best, int* matvecs) {
   if (!g) return fail(HOBI_ERR_STATE, "null group");

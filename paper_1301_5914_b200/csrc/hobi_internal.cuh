@@ -132,6 +132,9 @@ struct Comm {
   // fused epilogue + NVLink peer-store gather (hobi_comm_p2p_*)
   bool p2p = false;
   uint64_t epoch = 0;                 // operator applications gathered so far
+  bool p2p_only = false;              // hobi_comm_init_p2p: ranks without an NCCL communicator
+  bool p2p_fresh = false;             // receive area zeroed and not yet opened (hobi_comm_p2p_handle)
+  bool p2p_pending = false;           // hobi_matvec_p2p_phase: send half done, receive half due
   std::vector<void*> opened;          // peer areas opened through CUDA IPC
 };
 
@@ -265,5 +268,8 @@ int comm_allgather_bytes(hobi_ctx* c, const void* send, void* recv, size_t bytes
 // gathered [rank][2][m] slots -> out[0:nt] ++ out[nt:2nt] (hobi_sweep.cu)
 int gather_permute(hobi_ctx* c, double* out_dev);
 int p2p_check(hobi_ctx* c);
+// halves of the fused P2P gather (hobi_sweep.cu), for hobi_matvec_p2p_phase
+int matvec_p2p_send(hobi_ctx* c, const double* u_dev);
+int matvec_p2p_recv(hobi_ctx* c, double* out_dev);
 
 }  // namespace hobi

@@ -3,6 +3,8 @@
 // division): the Duffy singular swap, the charge source terms
 // (K-E) and the kernel-value test hook.  These touch O(N) pairs, so fidelity
 // to kernels.py beats instruction count here.
+#include <cstdlib>
+
 #include "hobi_internal.cuh"
 
 namespace hobi {
@@ -140,6 +142,81 @@ __global__ void singular_kernel(int64_t p0, int64_t p1, const int* __restrict__ 
   corr[2 * p + 1] = duf2 - reg2;
 }
 
+// The same correction with one warp per pair: lane m evaluates term m of the
+// pair's nq regular + nd Duffy points (looping when nq + nd > 32), the terms
+// land in shared memory, and lanes 0 and 1 sum the regular and the Duffy row
+// in numpy's order (numpy_row_sum) -- the identical operations in the
+// identical order as singular_kernel, so the output is bitwise the same, with
+// 20 evaluations in parallel instead of in series (HOBI_SINGULAR_SERIAL=1
+// selects the serial kernel, for the bitwise regression test).
+constexpr int kSingWarps = 4;          // pairs per 128-thread block
+constexpr int kSingMaxTerms = 16 + 64;  // nq <= 16, nd <= 64 (hobi_create)
+
+__global__ void __launch_bounds__(32 * kSingWarps) singular_warp_kernel(
+    int64_t p0, int64_t p1, const int* __restrict__ pair_vertex, const int* __restrict__ pair_face,
+    const int* __restrict__ pair_gverts, const int* __restrict__ faces, const double* __restrict__ vert,
+    const double* __restrict__ vnrm, const double* __restrict__ reg_pos, const double* __restrict__ reg_nrm,
+    const double* __restrict__ reg_w, const double* __restrict__ reg_bary, int nq,
+    const double* __restrict__ duf_pos, const double* __restrict__ duf_nrm, const double* __restrict__ duf_w,
+    const double* __restrict__ duf_bary, int nd, const double* __restrict__ u, int64_t nt, double er,
+    double kappa, double* __restrict__ corr) {
+  __shared__ double t1s[kSingWarps][kSingMaxTerms], t2s[kSingWarps][kSingMaxTerms];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p = p0 + (int64_t)blockIdx.x * kSingWarps + warp;
+  if (p >= p1) return;  // the whole warp leaves together
+  const int v = pair_vertex[p], f = pair_face[p];
+  const double x0 = vert[3 * v], x1 = vert[3 * v + 1], x2 = vert[3 * v + 2];
+  const double n0 = vnrm[3 * v], n1 = vnrm[3 * v + 1], n2 = vnrm[3 * v + 2];
+  const double* dphi = u + nt;
+  const int nterm = nq + nd;
+  for (int m = lane; m < nterm; m += 32) {
+    const double *y, *ny, *bary;
+    double w;
+    int ia, ib, ic;
+    if (m < nq) {  // regular point m of the rotation-0 element
+      const int64_t q = (int64_t)f * nq + m;
+      y = reg_pos + q * 3;
+      ny = reg_nrm + q * 3;
+      w = reg_w[q];
+      ia = faces[3 * f];
+      ib = faces[3 * f + 1];
+      ic = faces[3 * f + 2];
+      bary = reg_bary + 3 * m;
+    } else {  // Duffy point m - nq of the rotated element
+      const int mm = m - nq;
+      const int64_t q = p * nd + mm;
+      y = duf_pos + q * 3;
+      ny = duf_nrm + q * 3;
+      w = duf_w[q];
+      ia = pair_gverts[3 * p];
+      ib = pair_gverts[3 * p + 1];
+      ic = pair_gverts[3 * p + 2];
+      bary = duf_bary + 3 * mm;
+    }
+    K4 k = kernel_values_d(x0 - y[0], x1 - y[1], x2 - y[2], n0, n1, n2, ny[0], ny[1], ny[2], er, kappa);
+    double wp = w * interp3(u, ia, ib, ic, bary);
+    double wd = w * interp3(dphi, ia, ib, ic, bary);
+    t1s[warp][m] = k.k1 * wd + k.k2 * wp;
+    t2s[warp][m] = k.k3 * wd + k.k4 * wp;
+  }
+  __syncwarp();
+  double s1 = 0.0, s2 = 0.0;
+  if (lane < 2) {
+    const int off = lane == 0 ? 0 : nq, n = lane == 0 ? nq : nd;
+    const double* a1 = &t1s[warp][off];
+    const double* a2 = &t2s[warp][off];
+    numpy_row_sum(n, [&](int m, double& t1, double& t2) {
+      t1 = a1[m];
+      t2 = a2[m];
+    }, s1, s2);
+  }
+  const double duf1 = __shfl_sync(0xffffffffu, s1, 1), duf2 = __shfl_sync(0xffffffffu, s2, 1);
+  if (lane == 0) {
+    corr[2 * p] = duf1 - s1;
+    corr[2 * p + 1] = duf2 - s2;
+  }
+}
+
 // source_terms_at (kernels.py:159-178) + /eps1 (solver.py:402); one thread per
 // collocation point, charges staged through shared memory.
 __global__ void rhs_kernel(const double* __restrict__ pos, const double* __restrict__ nrm, int64_t lo,
@@ -187,10 +264,20 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1, cudaStream_t stream) {
   if (p1 <= p0) return 0;
-  singular_kernel<<<nblk(p1 - p0, 128), 128, 0, stream>>>(
-      p0, p1, c->pair_vertex.p, c->pair_face.p, c->pair_gverts.p, c->faces.p, c->vert.p, c->vnrm.p,
-      c->reg_pos.p, c->reg_nrm.p, c->reg_w.p, c->reg_bary.p, c->nq, c->duf_pos.p, c->duf_nrm.p,
-      c->duf_w.p, c->duf_bary.p, c->nd, u_dev, c->nt, c->phys.er, c->phys.kappa, c->corr.p);
+  static const bool serial = [] {
+    const char* e = getenv("HOBI_SINGULAR_SERIAL");
+    return e && e[0] == '1';
+  }();
+  if (serial)
+    singular_kernel<<<nblk(p1 - p0, 128), 128, 0, stream>>>(
+        p0, p1, c->pair_vertex.p, c->pair_face.p, c->pair_gverts.p, c->faces.p, c->vert.p, c->vnrm.p,
+        c->reg_pos.p, c->reg_nrm.p, c->reg_w.p, c->reg_bary.p, c->nq, c->duf_pos.p, c->duf_nrm.p,
+        c->duf_w.p, c->duf_bary.p, c->nd, u_dev, c->nt, c->phys.er, c->phys.kappa, c->corr.p);
+  else
+    singular_warp_kernel<<<nblk(p1 - p0, kSingWarps), 32 * kSingWarps, 0, stream>>>(
+        p0, p1, c->pair_vertex.p, c->pair_face.p, c->pair_gverts.p, c->faces.p, c->vert.p, c->vnrm.p,
+        c->reg_pos.p, c->reg_nrm.p, c->reg_w.p, c->reg_bary.p, c->nq, c->duf_pos.p, c->duf_nrm.p,
+        c->duf_w.p, c->duf_bary.p, c->nd, u_dev, c->nt, c->phys.er, c->phys.kappa, c->corr.p);
   c->launches++;
   HOBI_CUDA(cudaGetLastError());
   return 0;

@@ -774,8 +774,12 @@ std::vector<int2> make_groups(int n_src_tiles, int64_t tiles8) {
   if (n_src_tiles <= 0) return g;
   const int64_t want = std::max<int64_t>(1, (16 * 2 * 148 + tiles8 - 1) / tiles8);
   // large problems get at least 4 tiles (256 sources) per group, so the
-  // partial sums cost <= 1/16 B of HBM traffic per pair
-  const int floor = n_src_tiles >= 1024 ? 4 : 1;
+  // partial sums cost <= 1/16 B of HBM traffic per pair; from 4096 tiles
+  // (262,144 sources: config 4 and up) at least 32 tiles, which bounds the
+  // partial-sum buffer (2 doubles per row per group) to <= 2/2048 of the
+  // pair count in bytes -- config 4: ~170 groups, 111 MB instead of 645 / 423
+  // MB -- while an 8-way split still has >= 4 work items per CTA slot
+  const int floor = n_src_tiles >= 4096 ? 32 : n_src_tiles >= 1024 ? 4 : 1;
   const int B = (int)std::max<int64_t>(floor, (n_src_tiles + want - 1) / want);
   std::vector<int> tail;
   int tail_sum = 0;
@@ -891,11 +895,13 @@ int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi,
 }
 
 // Row split with the gather fused into the epilogue (peer stores + arrival
-// counters) instead of ncclAllGather + permutation.
-static int matvec_p2p(hobi_ctx* c, const double* u_dev, double* out_dev) {
+// counters) instead of ncclAllGather + permutation.  Two halves: the send
+// half computes this rank's rows and stores them into every rank's receive
+// area (bumping the arrival counters); the receive half waits for every
+// rank's arrivals of this epoch and copies the gathered vector out.
+int matvec_p2p_send(hobi_ctx* c, const double* u_dev) {
   const int64_t lo = c->lo, hi = c->hi;
   const int parity = (int)(c->comm.epoch & 1);
-  const unsigned long long target = c->comm.epoch / 2 + 1 + c->p2p_extra;  // arrivals per rank
   int rc;
   const bool hobi = c->scheme == kHobi;
   if (hi > lo) {
@@ -911,19 +917,37 @@ static int matvec_p2p(hobi_ctx* c, const double* u_dev, double* out_dev) {
       hobi ? c->pair_starts.p : nullptr, u_dev, c->nt, lo, hi,
       c->phys.diag1, c->phys.diag2, c->p2p_peers.p, c->comm.nranks, c->comm.rank, parity,
       c->p2p_done.p);
+  c->launches++;
+  HOBI_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int matvec_p2p_recv(hobi_ctx* c, double* out_dev) {
+  const int parity = (int)(c->comm.epoch & 1);
+  const unsigned long long target = c->comm.epoch / 2 + 1 + c->p2p_extra;  // arrivals per rank
   p2p_wait_copy_kernel<<<std::max(1u, nblk(2 * c->nt, 1024)), 256, 0, c->stream>>>(
       c->p2p_area.p, c->nt, c->comm.nranks, parity, target, c->p2p_timeout_ns, c->p2p_err_dev, out_dev);
-  c->launches += 2;
+  c->launches++;
   HOBI_CUDA(cudaGetLastError());
   c->comm.epoch++;
   return 0;
 }
 
+static int matvec_p2p(hobi_ctx* c, const double* u_dev, double* out_dev) {
+  int rc = matvec_p2p_send(c, u_dev);
+  return rc ? rc : matvec_p2p_recv(c, out_dev);
+}
+
 int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
   int rc;
-  if (c->comm.p2p) return matvec_p2p(c, u_dev, out_dev);
+  if (c->comm.p2p) {
+    if (c->comm.p2p_pending) return fail(HOBI_ERR_STATE, "a P2P send phase is pending (hobi_matvec_p2p_phase)");
+    return matvec_p2p(c, u_dev, out_dev);
+  }
   if (c->comm.nranks == 1 && !c->comm.nccl)
     return matvec_rows_device(c, u_dev, 0, c->nt, out_dev, out_dev + c->nt);
+  if (!c->comm.emulated && !c->comm.nccl)
+    return fail(HOBI_ERR_STATE, "row split without a gather: the P2P communicator's peer areas are not open");
   const int64_t m = c->gather_m;
   if (c->comm.emulated) {  // every rank's rows, computed here, in the gather layout
     for (int r = 0; r < c->comm.nranks; ++r) {

@@ -432,7 +432,8 @@ class GpuOperator:
     first): every extra device gets a replica context and the native group
     operator gathers the rows over peer copies.  With fewer GPUs the split is
     emulated on the problem's GPU (same gather layout and permutation as the
-    NCCL path).  Either way the result is bitwise that of one GPU.
+    NCCL path) and a ``RuntimeWarning`` says so; ``placement`` reports which
+    of the three ran.  Either way the result is bitwise that of one GPU.
     ``devices`` may repeat a device (replicas sharing it) -- the test hook for
     the group path on a one-GPU machine.
     """
@@ -443,6 +444,7 @@ class GpuOperator:
         self._emulated = False
         self._group = None
         self._replicas = []
+        self._workers = 1
         lib = N.load()
         if problem.world != 1 or problem.n_collocation == 0:
             return
@@ -461,8 +463,35 @@ class GpuOperator:
             _raise(lib.hobi_group_create(members, len(devices), C.byref(grp)))
             self._group = grp.value
         elif workers > 1:
+            import warnings
+
+            warnings.warn(f"workers={workers} but only {N.device_count()} GPU(s) visible: the {workers}-way "
+                          f"row split is emulated on GPU {problem.device} (same rows, one device)",
+                          RuntimeWarning, stacklevel=3)
             _raise(lib.hobi_emulate_ranks(problem.handle, workers))
             self._emulated = True
+        self._workers = workers
+
+    @property
+    def placement(self) -> dict:
+        """How the rows run: ``mode`` is "single", "group" (one process, one
+        context per device, ``devices`` lists them), "emulated" (a workers-way
+        split on one GPU) or "ranks" (torch.distributed, one process per GPU)."""
+        if self._problem.world != 1:
+            return {"mode": "ranks", "workers": self._problem.world, "devices": [self._problem.device]}
+        if self._group is not None:
+            n = len(self._replicas) + 1
+            devs = (C.c_int * n)()
+            N.check(N.load().hobi_group_info(self._group, None, devs, None, None, None))
+            return {"mode": "group", "workers": n, "devices": list(devs)}
+        if self._emulated:
+            return {"mode": "emulated", "workers": self._workers, "devices": [self._problem.device]}
+        return {"mode": "single", "workers": 1, "devices": [self._problem.device]}
+
+    @property
+    def member_handles(self) -> list:
+        """Native contexts of a group (leader first); [problem.handle] otherwise."""
+        return [self._problem.handle] + [h.ptr for h in self._replicas]
 
     @property
     def problem(self):
