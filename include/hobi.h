@@ -285,6 +285,24 @@ int hobi_sweep_layout(hobi_ctx* ctx, int* n_groups, int64_t* n_sources_padded);
 int hobi_msms_parse(const char* vert, int64_t vert_len, const char* face, int64_t face_len, double* vdata,
                     int64_t vert_cap, int64_t* faces, int64_t face_cap, int64_t* n_vert, int64_t* n_face);
 
+/*
+ * Analytic Kirkwood validator on the device (kirkwood.py:159-220; the
+ * O(points x charges x terms) sums of kirkwood_series).  The caller supplies
+ * what the reference computes per charge: unit directions (nc, 3), radii
+ * rho (nc), and rows of nterms coefficients per charge.
+ * hobi_kirkwood_traces: phi[i] = sum_k coef_phi[k] . P(rad_i . u_k) and the
+ * same for dphi (kirkwood.py:193-203), P by the reference's recurrence
+ * (kirkwood.py:59-71), cos = 1 for a charge at the centre.
+ * hobi_kirkwood_energy_terms: terms[j] = 1/2 q_j sum_k sum_n
+ * reac[k,n] rpow[j,n] P_n(u_k . u_j) (kirkwood.py:180-188); the energy is
+ * 4 pi 332.0716 sum_j terms[j].  nterms <= 256.
+ */
+int hobi_kirkwood_traces(int device, const double* points, int64_t m, const double* units, const double* rho,
+                         int64_t nc, const double* coef_phi, const double* coef_dphi, int nterms, double* phi,
+                         double* dphi);
+int hobi_kirkwood_energy_terms(int device, const double* units, const double* q, int64_t nc, const double* reac,
+                               const double* rpow, int nterms, double* terms);
+
 /* Regular pairs per full matvec (N_v x N_f x nq for hobi), for throughput. */
 int hobi_pairs_per_matvec(hobi_ctx* ctx, double* pairs);
 

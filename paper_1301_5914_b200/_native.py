@@ -79,6 +79,9 @@ SIGNATURES = {
     "hobi_comm_p2p_open": (C.c_int, [_ctxp, C.POINTER(C.c_ubyte), C.c_int, C.c_int]),
     "hobi_comm_init_p2p": (C.c_int, [_ctxp, C.c_int, C.c_int]),
     "hobi_matvec_p2p_phase": (C.c_int, [_ctxp, _dp, _dp, C.c_int]),
+    "hobi_kirkwood_traces": (C.c_int, [C.c_int, _dp, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp, C.c_int, _dp,
+                                       _dp]),
+    "hobi_kirkwood_energy_terms": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _dp, _dp, C.c_int, _dp]),
     "hobi_timing_reset": (C.c_int, [_ctxp]),
     "hobi_timing": (C.c_int, [_ctxp, _dp, _i64p, _i64p]),
     "hobi_pairs_per_matvec": (C.c_int, [_ctxp, _dp]),

@@ -29,6 +29,7 @@ UNITS = {
     "hobi_msms.cu": [],
     "hobi_geometry.cu": ["-fmad=false"],
     "hobi_literal.cu": ["-fmad=false"],
+    "hobi_kirkwood.cu": ["-fmad=false"],
 }
 HEADERS = ["hobi_internal.cuh", "hobi_fastmath.cuh", "hobi_default_rules.inc"]
 

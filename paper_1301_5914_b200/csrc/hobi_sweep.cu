@@ -353,6 +353,9 @@ __global__ void __launch_bounds__(kEpiRows* kEpiSlices) epilogue_kernel(
   const int64_t v = lo + (int64_t)blockIdx.x * kEpiRows + threadIdx.x;
   const int64_t vv = v < hi ? v : hi - 1;
   double a1 = 0.0, a2 = 0.0;
+  // unrolled so the independent partial loads issue back to back (the adds
+  // keep their group order: same bits, a fraction of the load latency)
+#pragma unroll 4
   for (int g = threadIdx.y; g < n_groups; g += kEpiSlices) {
     a1 += part[(2 * (int64_t)g) * ldp + vv];
     a2 += part[(2 * (int64_t)g + 1) * ldp + vv];
@@ -392,6 +395,7 @@ __global__ void __launch_bounds__(kEpiRows* kEpiSlices) epilogue_p2p_kernel(
   const int64_t v = lo + (int64_t)blockIdx.x * kEpiRows + threadIdx.x;
   const int64_t vv = v < hi ? v : hi - 1;
   double a1 = 0.0, a2 = 0.0;
+#pragma unroll 4
   for (int g = threadIdx.y; hi > lo && g < n_groups; g += kEpiSlices) {
     a1 += part[(2 * (int64_t)g) * ldp + vv];
     a2 += part[(2 * (int64_t)g + 1) * ldp + vv];
@@ -774,12 +778,12 @@ std::vector<int2> make_groups(int n_src_tiles, int64_t tiles8) {
   if (n_src_tiles <= 0) return g;
   const int64_t want = std::max<int64_t>(1, (16 * 2 * 148 + tiles8 - 1) / tiles8);
   // large problems get at least 4 tiles (256 sources) per group, so the
-  // partial sums cost <= 1/16 B of HBM traffic per pair; from 4096 tiles
-  // (262,144 sources: config 4 and up) at least 32 tiles, which bounds the
-  // partial-sum buffer (2 doubles per row per group) to <= 2/2048 of the
-  // pair count in bytes -- config 4: ~170 groups, 111 MB instead of 645 / 423
-  // MB -- while an 8-way split still has >= 4 work items per CTA slot
-  const int floor = n_src_tiles >= 4096 ? 32 : n_src_tiles >= 1024 ? 4 : 1;
+  // partial sums cost <= 1/16 B of HBM traffic per pair.  Coarser groups
+  // shrink the partial-sum buffer but starve split ranks of work items: a
+  // 32-tile floor (config 4: 169 groups, 111 MB instead of 645 / 423 MB) cut
+  // the one-GPU model of a 4- and 8-way split of config 4 from 98.1% and 96.1% to 88.5%
+  // and 85.5% efficiency (profiles/r02_group_floor.md), so the floor stays 4.
+  const int floor = n_src_tiles >= 1024 ? 4 : 1;
   const int B = (int)std::max<int64_t>(floor, (n_src_tiles + want - 1) / want);
   std::vector<int> tail;
   int tail_sum = 0;

@@ -4,8 +4,14 @@ The validator that follows a solve for configs 1-2,
 restated from the reference (``pbbem/kirkwood.py:59-263``): Laplace
 harmonics inside, modified spherical Bessel functions k_n(kappa r) outside,
 matched by continuity of phi and eps dphi/dr at r = a.  Vectorised over
-charges and evaluation points (the reference loops over charges); host numpy,
-O(N_c * N_points * n_terms).
+charges and evaluation points (the reference loops over charges).
+
+Two backends: "gpu" (default) runs the O(N_points x N_c x n_terms) Legendre
+sums -- the surface traces (kirkwood.py:193-203) and the charge-charge energy
+(kirkwood.py:180-188) -- in sm_100a kernels (csrc/hobi_kirkwood.cu) behind
+the C ABI and raises without a device, like every other product path;
+"host" keeps the vectorised numpy restatement for CPU-only validation.  The
+O(N_c x n_terms) coefficients are computed on the host either way.
 """
 
 from __future__ import annotations
@@ -87,10 +93,55 @@ def _directions(v):
     return r, u
 
 
-def kirkwood_series(problem: SphereProblem, n_terms: int = 40) -> KirkwoodSolution:
-    """Multipole solution for arbitrary interior charges (kirkwood.py:159-220)."""
+def _gpu_traces(coef_phi, coef_dphi, units, rho, nmax):
+    """Both traces at a set of points through hobi_kirkwood_traces (one launch)."""
+    from . import _native as N
+    from .solver import _device_index, _raise
+
+    units, rho = N.f64(units), N.f64(rho)
+    c1, c2 = N.f64(coef_phi), N.f64(coef_dphi)
+    nc = rho.size
+
+    def evaluate(points):
+        pts = N.f64(points)
+        single = pts.ndim == 1
+        pts = np.ascontiguousarray(pts.reshape(-1, 3))
+        m = pts.shape[0]
+        phi, dphi = np.empty(m), np.empty(m)
+        N.require_device()
+        _raise(N.load().hobi_kirkwood_traces(_device_index(), N.dptr(pts), m, N.dptr(units), N.dptr(rho), nc,
+                                             N.dptr(c1), N.dptr(c2), nmax + 1, N.dptr(phi), N.dptr(dphi)))
+        return (phi[0], dphi[0]) if single else (phi, dphi)
+
+    return evaluate
+
+
+def _gpu_energy(units, q, reac, rpow, nmax):
+    from . import _native as N
+    from .solver import _device_index, _raise
+
+    q = N.f64(q)
+    terms = np.empty(q.size)
+    if q.size:
+        N.require_device()
+        _raise(N.load().hobi_kirkwood_energy_terms(_device_index(), N.dptr(N.f64(units)), N.dptr(q), q.size,
+                                                   N.dptr(N.f64(reac)), N.dptr(N.f64(rpow)), nmax + 1,
+                                                   N.dptr(terms)))
+    energy = 0.0
+    for t in terms:  # charge order, like the reference's loop over j
+        energy += float(t)
+    return energy
+
+
+def kirkwood_series(problem: SphereProblem, n_terms: int = 40, backend: str = "gpu") -> KirkwoodSolution:
+    """Multipole solution for arbitrary interior charges (kirkwood.py:159-220).
+
+    ``backend="gpu"`` evaluates the energy and the traces on the device
+    (no CPU fallback: raises without one); ``"host"`` uses numpy."""
     if n_terms < 1:
         raise ValueError(f"n_terms must be >= 1, got {n_terms}")
+    if backend not in ("gpu", "host"):
+        raise ValueError(f"backend must be 'gpu' or 'host', got {backend!r}")
     nmax = n_terms - 1
     a, p = problem.radius, problem.params
     q = problem.charges.charges
@@ -102,14 +153,24 @@ def kirkwood_series(problem: SphereProblem, n_terms: int = 40) -> KirkwoodSoluti
     rpow[:, 0] = 1.0
     alpha = q[:, None] * rpow / (FOUR_PI * p.eps1)
     reac = alpha * (a ** -(2 * n + 1.0) * (p.eps2 * ell + (n + 1) * p.eps1) / (n * p.eps1 - p.eps2 * ell))
-    # E = 1/2 sum_j q_j phi_reac(y_j): P_n(u_j . u_k) for all charge pairs at once
-    pn = legendre_table(nmax, np.clip(units @ units.T, -1.0, 1.0)) if len(q) else np.zeros((nmax + 1, 0, 0))
-    energy = 0.0
-    for j in range(len(q)):
-        energy += 0.5 * q[j] * float((reac * rpow[j][None, :] * pn[:, :, j].T).sum())
-    energy *= FOUR_PI * KCAL_MOL_PER_E2_ANG
     coef_phi = alpha * a ** -(n + 1.0) + reac * a**n
     coef_dphi = -(n + 1.0) * alpha * a ** -(n + 2.0) + n * reac * a ** (n - 1.0)
+    if backend == "gpu":
+        energy = _gpu_energy(units, q, reac, rpow, nmax)
+        energy *= FOUR_PI * KCAL_MOL_PER_E2_ANG
+        both = _gpu_traces(coef_phi, coef_dphi, units, rho, nmax)
+
+        def trace_gpu(which):
+            return lambda points: both(points)[which]
+
+        phi_fn, dphi_fn = trace_gpu(0), trace_gpu(1)
+    else:
+        # E = 1/2 sum_j q_j phi_reac(y_j): P_n(u_j . u_k) for all charge pairs at once
+        pn = legendre_table(nmax, np.clip(units @ units.T, -1.0, 1.0)) if len(q) else np.zeros((nmax + 1, 0, 0))
+        energy = 0.0
+        for j in range(len(q)):
+            energy += 0.5 * q[j] * float((reac * rpow[j][None, :] * pn[:, :, j].T).sum())
+        energy *= FOUR_PI * KCAL_MOL_PER_E2_ANG
 
     def trace(coef):
         def evaluate(points):
@@ -129,7 +190,9 @@ def kirkwood_series(problem: SphereProblem, n_terms: int = 40) -> KirkwoodSoluti
         tail = float(np.where(last > 0.0, last / np.maximum(prev, 1e-300), 0.0).max())
     else:
         tail = 1.0 if np.abs(coef_phi).max(initial=0.0) > 0.0 else 0.0
-    return KirkwoodSolution(energy=energy, phi=trace(coef_phi), dphi_dn=trace(coef_dphi),
+    if backend == "host":
+        phi_fn, dphi_fn = trace(coef_phi), trace(coef_dphi)
+    return KirkwoodSolution(energy=energy, phi=phi_fn, dphi_dn=dphi_fn,
                             tail_ratio=tail, converged=tail <= 0.99, n_terms=n_terms)
 
 
