@@ -34,9 +34,11 @@ quadrature point): N_v * 4 N_f = 1.342e10 pairs per step.
             exchange bytes per matvec and the step time not spent computing.
 `solve`   : one full GMRES solve of the config (restart 20, tol 1e-6) through
             the public API (wall clock, includes every matvec).
-`cpu_baseline`: the numpy restatement of the reference (oracle/, a "port";
-            the reference itself is Python and cannot travel to the box) on a
-            bounded row sample of the same workload, fork pool over all cores.
+`cpu_baseline`: the numpy restatement of the reference (oracle/, a "port")
+            on a bounded row sample of the same workload, fork pool over all
+            cores.  `--impl reference` times the unmodified reference
+            (pbbem pip-installed under baseline/_ref, which travels with the
+            repo) on the same kind of sample, falling back to the port.
 """
 
 from __future__ import annotations
@@ -204,8 +206,55 @@ def _cpu_sample(cfg, u, rows_hint, target_s=15.0):
     return {"pairs": float(rows) * nsrc, "seconds": dt, "rows": rows, "workers": workers}
 
 
+def _reference_rows(cfg, workers):
+    """The reference's own row-range unit on a fork pool of `workers`.
+
+    Prefers the unmodified reference package installed under baseline/_ref
+    (pip install --no-deps --target baseline/_ref of the reference's pkg/):
+    pbbem.solver.discretize, then its _Operator fork pool running
+    _range_task / _apply_range (solver.py:278-367, 424-459) over the sampled
+    rows split with its own partition_targets -- kind "reference".  Without
+    that install, the numpy restatement under oracle/ (kind "port").
+    Returns (rows(u, lo, hi), close(), kind, label, setup_seconds)."""
+    t0 = time.perf_counter()
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    m = cfg.mesh
+    if os.path.isdir(os.path.join(ref_dir, "pbbem")):
+        sys.path.insert(0, ref_dir)
+        from pbbem import kernels as rk
+        from pbbem import mesh as rm
+        from pbbem import solver as rs
+
+        prob = rs.discretize(rm.FlatMesh(vertices=m.vertices, normals=m.normals, faces=m.faces),
+                             rk.PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa),
+                             rm.ChargeSystem(positions=cfg.charges.positions, charges=cfg.charges.charges),
+                             rs.SolverConfig(scheme="hobi", workers=workers))
+        op = rs._Operator(prob, workers)
+
+        def rows(u, lo, hi):
+            if op._pool is None:
+                return rs._apply_range(prob, u, lo, hi)
+            parts = rs.partition_targets(hi - lo, workers)
+            return op._pool.starmap(rs._range_task, [(op._token, u, lo + a, lo + b) for a, b in parts])
+
+        return (rows, op.close, "reference",
+                f"unmodified pbbem (baseline/_ref) _Operator fork pool of {workers} workers, _range_task",
+                time.perf_counter() - t0)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hobi_oracle as O
+
+    prob = O.discretize(m.vertices, m.normals, m.faces, cfg.eps1, cfg.eps2, cfg.kappa, check=False)
+    op = O.PoolOperator(prob, workers)
+    op.__enter__()
+    return (op.rows, lambda: op.__exit__(None, None, None), "port",
+            f"oracle/hobi_oracle.py (numpy port of the reference) fork pool of {workers} workers",
+            time.perf_counter() - t0)
+
+
 def run_reference(a):
-    """--impl reference: the reference algorithm on host cores (oracle port), rank 0 only."""
+    """--impl reference: the reference's CPU implementation of the path on the
+    host cores (unmodified pbbem from baseline/_ref, else the oracle port),
+    rank 0 only."""
     rank, world, _ = _dist()
     if rank != 0:
         return 0
@@ -213,24 +262,22 @@ def run_reference(a):
 
     cfg = baseline_config(a.config)
     nv, nf, nq = cfg.mesh.n_vertices, cfg.mesh.n_faces, 4
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import hobi_oracle as O
-
     u = np.random.default_rng(0).standard_normal(2 * nv)
-    m = cfg.mesh
-    prob = O.discretize(m.vertices, m.normals, m.faces, cfg.eps1, cfg.eps2, cfg.kappa, check=False)
     workers = os.cpu_count() or 1
     rows = a.cpu_rows or max(2 * workers, 256)
     nsrc = nf * nq
     times = []
-    with O.PoolOperator(prob, workers) as op:
+    run_rows, close, kind, label, setup_s = _reference_rows(cfg, workers)
+    try:
         for i in range(a.warmup + a.steps):
             lo = (i * rows) % max(1, nv - rows)
             t0 = time.perf_counter()
-            op.rows(u, lo, lo + rows)
+            run_rows(u, lo, lo + rows)
             dt = time.perf_counter() - t0
             if i >= a.warmup:
                 times.append(dt)
+    finally:
+        close()
     total = sum(times)
     value = a.steps * rows * nsrc / total
     line = {
@@ -238,9 +285,9 @@ def run_reference(a):
         "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _workload(cfg, nv, nf, nq, a.gpus), "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": workers, "kind": "port",
-                         "sample": f"{rows} target rows x {nsrc} sources per step (rows rotate), "
-                                   f"oracle/hobi_oracle.py fork pool of {workers} workers"},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": workers, "kind": kind,
+                         "sample": f"{rows} target rows x {nsrc} sources per step (rows rotate), {label}; "
+                                   f"setup (discretize) {setup_s:.1f} s untimed"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
