@@ -111,6 +111,8 @@ def plan_launch(gpus: int, env, visible) -> str:
         return "torchrun" if world > 1 or env.get("HOBI_FORCE_NCCL") == "1" else "single"
     if gpus == 1:
         return "single"
+    if env.get("HOBI_BENCH_GROUP_SHARED") == "1":
+        return "group-shared"  # test hook: N group members on GPU 0, labelled as such
     n = visible()
     if n < gpus:
         raise LaunchError(f"--gpus {gpus} requested but only {n} GPU(s) are visible; "
@@ -343,12 +345,13 @@ class _RankRunner:
 class _GroupRunner(_RankRunner):
     """One process driving N GPUs through the native group operator."""
 
-    def __init__(self, a, lib, N, prob, op):
+    def __init__(self, a, lib, N, prob, op, shared=False):
         self.a, self.use_dist, self.lib, self.N = a, False, lib, N
         self.prob, self.world, self.rank = prob, a.gpus, 0
         self.group_op = op
         pl = op.placement
-        if pl["mode"] != "group" or pl["workers"] != a.gpus or len(set(pl["devices"])) != a.gpus:
+        distinct = 1 if shared else a.gpus
+        if pl["mode"] != "group" or pl["workers"] != a.gpus or len(set(pl["devices"])) != distinct:
             raise LaunchError(f"group operator did not place {a.gpus} GPUs: {pl}")
         self.handles = op.member_handles
         self.devices = pl["devices"]
@@ -407,6 +410,9 @@ def run_ours(a):
 
         torch.cuda.set_device(local)
         dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
+    shared = mode == "group-shared"
+    if shared:
+        mode = "group"
     if mode == "group":
         os.environ["HOBI_DEVICE"] = "0"
         local = 0
@@ -422,14 +428,15 @@ def run_ours(a):
     scfg = SolverConfig(workers=1, restart=cfg.restart, tolerance=cfg.tol)
     prob = discretize(cfg.mesh, params, cfg.charges, scfg)
     if mode == "group":
-        run = _GroupRunner(a, lib, N, prob, GpuOperator(prob, workers=a.gpus))
+        devs = [0] * a.gpus if shared else None
+        run = _GroupRunner(a, lib, N, prob, GpuOperator(prob, workers=a.gpus, devices=devs), shared)
         world = a.gpus
     else:
         run = _RankRunner(a, use_dist, lib, N, prob, world, rank)
     nv, nf, nq = cfg.mesh.n_vertices, cfg.mesh.n_faces, 4
     pairs_step = float(nv) * nf * nq
     peaks = []
-    for d in run.devices:
+    for d in sorted(set(run.devices)):
         pk = C.c_double(0.0)
         N.check(lib.hobi_probe_fp64_tflops(d, 300.0, C.byref(pk)))
         peaks.append(pk.value)
@@ -443,7 +450,7 @@ def run_ours(a):
     barrier()
     for h in run.handles:
         N.check(lib.hobi_timing_reset(h))
-    with _Clocks(run.devices) as clocks:
+    with _Clocks(sorted(set(run.devices))) as clocks:
         run.bench(N.dptr(u), N.dptr(out), a.steps, 0, ms)
     barrier()
     launches_total, members = 0, []
@@ -496,7 +503,7 @@ def run_ours(a):
     try:
         import torch
 
-        for d in run.devices:
+        for d in sorted(set(run.devices)):
             flush.append(torch.empty(64 << 20, dtype=torch.float64, device=f"cuda:{d}"))
     except Exception:  # noqa: BLE001
         flush = []
@@ -512,7 +519,7 @@ def run_ours(a):
         for f in flush:
             f.fill_(1.0)
         if flush:
-            for d in run.devices:
+            for d in sorted(set(run.devices)):
                 torch.cuda.synchronize(d)
         t0 = time.perf_counter()
         op_api(u_api, out=out_api)
@@ -663,6 +670,10 @@ def run_ours(a):
             "split_model": split_model,
             "cpu_baseline": cpu,
         }
+        if shared:
+            line["n_gpus"] = 1
+            line["test_hook"] = (f"HOBI_BENCH_GROUP_SHARED=1: {a.gpus} group members share GPU 0 -- exercises "
+                                 f"the {a.gpus}-way group code path, NOT an {a.gpus}-GPU measurement")
         print(json.dumps(line), flush=True)
     if mode == "group":
         run.group_op.close()

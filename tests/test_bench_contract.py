@@ -51,6 +51,7 @@ def test_plan_launch_never_downgrades():
     assert bench.plan_launch(4, {"WORLD_SIZE": "4", "RANK": "1"}, none) == "torchrun"
     assert bench.plan_launch(1, {"WORLD_SIZE": "1", "RANK": "0"}, none) == "single"
     assert bench.plan_launch(1, {"WORLD_SIZE": "1", "RANK": "0", "HOBI_FORCE_NCCL": "1"}, none) == "torchrun"
+    assert bench.plan_launch(2, {"HOBI_BENCH_GROUP_SHARED": "1"}, one) == "group-shared"
     for gpus, env, vis in ((2, {}, one), (8, {}, none), (2, {"WORLD_SIZE": "4"}, eight),
                            (4, {"WORLD_SIZE": "1"}, eight), (0, {}, eight)):
         with pytest.raises(bench.LaunchError) as exc:

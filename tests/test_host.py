@@ -162,3 +162,14 @@ def test_config_table():
     assert c2.mesh.n_faces == 5120 and len(c2.charges) == 8
     assert np.all(np.abs(c2.charges.charges) == 1.0)
     assert np.all(np.linalg.norm(c2.charges.positions, axis=1) < 1.2)
+
+
+def test_cli_restart_flag_is_honoured_even_at_100():
+    from paper_1301_5914_b200.cli import _restart, build_parser
+
+    assert _restart(None, None) == 100
+    assert _restart(None, 4) == 20  # BASELINE config 4's restart
+    assert _restart(100, 4) == 100  # an explicit --restart 100 wins over the config
+    assert _restart(7, None) == 7
+    args = build_parser().parse_args(["solve", "--config", "4"])
+    assert args.restart is None
