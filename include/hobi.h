@@ -325,6 +325,11 @@ int hobi_bench(hobi_ctx* ctx, const double* u, double* out, int steps, int mode,
 int hobi_bench_rows(hobi_ctx* ctx, const double* u, int64_t lo, int64_t hi, int steps, int flush_l2,
                     double* ms);
 
+/* Test hook: the device hypot used by the device-driven GMRES cycle (glibc's
+ * double hypot restated, so Givens rotations round like np.hypot,
+ * solver.py:551) on n argument pairs; out[i] = hypot(a[i], b[i]). */
+int hobi_hypot_check(int device, const double* a, const double* b, int64_t n, double* out);
+
 /* DFMA throughput probe (FP64 roofline denominator), TFLOP/s over ~`ms` ms. */
 int hobi_probe_fp64_tflops(int device, double ms, double* tflops);
 

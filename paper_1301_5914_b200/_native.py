@@ -82,6 +82,7 @@ SIGNATURES = {
     "hobi_kirkwood_traces": (C.c_int, [C.c_int, _dp, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp, C.c_int, _dp,
                                        _dp]),
     "hobi_kirkwood_energy_terms": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _dp, _dp, C.c_int, _dp]),
+    "hobi_hypot_check": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _dp]),
     "hobi_timing_reset": (C.c_int, [_ctxp]),
     "hobi_timing": (C.c_int, [_ctxp, _dp, _i64p, _i64p]),
     "hobi_pairs_per_matvec": (C.c_int, [_ctxp, _dp]),

@@ -617,6 +617,20 @@ struct CtxOperator : DeviceOperator {
     int rc = p2p_check(c);  // GMRES has synchronised on the previous application
     return rc ? rc : matvec_full_device(c, in, out);
   }
+  // One unsplit context (no collective, no P2P epochs, no emulated split):
+  // its matvec is stream work only, so GMRES may replay it from a graph.
+  uint64_t graph_key() override {
+    if (c->comm.nranks != 1 || c->comm.nccl || c->comm.p2p || c->comm.emulated) return 0;
+    if (getenv("HOBI_GMRES_GRAPH") && getenv("HOBI_GMRES_GRAPH")[0] == '0') return 0;
+    return reinterpret_cast<uintptr_t>(c) ^ ((uint64_t)(c->sweep_variant + 1) << 48) ^
+           ((uint64_t)c->variant_pinned << 60);
+  }
+  bool saved_timing = true;
+  void begin_capture() override {
+    saved_timing = c->timing;
+    c->timing = false;
+  }
+  void end_capture() override { c->timing = saved_timing; }
 };
 
 struct HostOperator : DeviceOperator {

@@ -140,9 +140,38 @@ struct Comm {
 
 // Device workspaces kept by a context across calls: cudaMalloc/cudaFree on
 // every solve showed 0.1-0.3 s stalls on the B200 hosts.
+// Inner-cycle state of the device-driven Arnoldi loop (hobi_gmres.cu).
+struct GmresState {
+  int j, total, m, max_it;
+  double norm_b, tol;
+};
+
+// An instantiated CUDA graph, destroyed with its owner.
+struct GraphHolder {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t key = 0;           // DeviceOperator::graph_key() it was captured for
+  int64_t step_launches = 0;  // kernels one loop iteration launches
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    key = 0;
+  }
+  ~GraphHolder() { reset(); }
+};
+
 struct GmresWorkspace {
   DevBuf<double> V, w, x, r, b, part, hcol, nrm, y;
   HostBuf<double> hcol_h, nrm_h;  // pinned landing slots of the per-step reads
+  // device-driven inner cycle: iterate copy, rotated Hessenberg, Givens
+  // factors, rhs g, loop state (+ pinned mirrors) and the cycle's graph
+  DevBuf<double> vin, H, cs, sn, g;
+  DevBuf<GmresState> st;
+  HostBuf<GmresState> st_h;
+  HostBuf<double> H_h, g_h;
+  GraphHolder cycle;
   int64_t n = -1, ldv = 0;
   int m = -1, grid = 1;
 };
@@ -254,6 +283,14 @@ int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1, cu
 // GMRES (hobi_gmres.cu)
 struct DeviceOperator {
   virtual int apply(const double* in_dev, double* out_dev) = 0;
+  // Non-zero when apply() is a pure sequence of stream work on the GMRES
+  // stream that may be captured into a CUDA graph and replayed; the value
+  // changes whenever the captured work would (operator, tiling, ...).
+  virtual uint64_t graph_key() { return 0; }
+  // Bracket the capture: the operator stops recording its instrumentation
+  // events (a captured cudaEventRecord never fires on replay).
+  virtual void begin_capture() {}
+  virtual void end_capture() {}
   virtual ~DeviceOperator() {}
 };
 int gmres_device(int device, cudaStream_t stream, int64_t n, DeviceOperator* op,

@@ -1,4 +1,5 @@
 set -x
-timeout 1200 python -m pytest tests/test_gpu_bench_paths.py tests/test_gpu_kirkwood.py -q -p no:cacheprovider > gpurun_out/r2_t3.log 2>&1
-timeout 900 python bench.py > gpurun_out/r2_b5.json 2> gpurun_out/r2_b5.err
-timeout 900 python bench.py --impl reference > gpurun_out/r2_ref5.json 2> gpurun_out/r2_ref5.err
+timeout 900 python -m pytest tests/test_gpu_gmres_graph.py tests/test_hypot.py -x -q -p no:cacheprovider > gpurun_out/r2_t4.log 2>&1
+timeout 300 python tools/solve_table.py 1 2 3 4 > gpurun_out/r2_solve_table3.jsonl 2>&1
+HOBI_GMRES_GRAPH=0 timeout 300 python tools/solve_table.py 1 2 3 4 > gpurun_out/r2_solve_table3_nograph.jsonl 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r2_tall3.log 2>&1
