@@ -158,3 +158,30 @@ def test_c_example_compiles():
                               os.path.join(ROOT, "examples", "c_solve.c"), "-L", os.path.dirname(N.LIB_PATH),
                               "-lhobi", "-o", os.path.join(tmp, "c_solve")], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
+
+
+def test_round2_entry_points_validate_arguments_without_a_device():
+    """The round-2 C-ABI entries reject bad handles and sizes before they touch
+    a device (status codes, no crash), on any machine."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_1301_5914_b200 import _native as N
+
+    lib = N.load()
+    z = np.zeros(4)
+    assert lib.hobi_kirkwood_traces(0, N.dptr(z), 1, N.dptr(z), N.dptr(z), 1, N.dptr(z), N.dptr(z), 0,
+                                    N.dptr(z), N.dptr(z)) == N.HOBI_ERR_VALUE
+    assert lib.hobi_kirkwood_traces(0, N.dptr(z), 0, N.dptr(z), N.dptr(z), 1, N.dptr(z), N.dptr(z), 3,
+                                    N.dptr(z), N.dptr(z)) == N.HOBI_OK  # nothing to evaluate
+    assert lib.hobi_kirkwood_energy_terms(0, N.dptr(z), N.dptr(z), -1, N.dptr(z), N.dptr(z), 3,
+                                          N.dptr(z)) == N.HOBI_ERR_VALUE
+    assert lib.hobi_hypot_check(0, N.dptr(z), N.dptr(z), -1, N.dptr(z)) == N.HOBI_ERR_VALUE
+    assert lib.hobi_comm_init_p2p(None, 2, 0) == N.HOBI_ERR_STATE
+    assert lib.hobi_matvec_p2p_phase(None, N.dptr(z), N.dptr(z), 0) == N.HOBI_ERR_STATE
+    assert lib.hobi_group_info(None, None, None, None, None, None) == N.HOBI_ERR_STATE
+    ms = np.zeros(1)
+    assert lib.hobi_group_bench(None, N.dptr(z), N.dptr(z), 1, 0, 0, N.dptr(ms)) == N.HOBI_ERR_STATE
+    assert "null" in N.last_error()
+    del C
