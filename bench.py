@@ -371,15 +371,38 @@ class _GroupRunner(_RankRunner):
         return self.group_op
 
 
-def _sweep_source_hash():
-    """SHA-256 of the sweep kernel's sources: stamps the committed ncu traffic."""
-    import hashlib
+# the default config-4 sweep instantiation, sweep_kernel<kScreened, FULL, !SELF, R=7, MINB=2, UNROLL=3, STEP>
+MAIN_SWEEP = "sweep_kernelILi1ELb1ELb0ELi7ELi2ELi3ELb1E"
 
-    h = hashlib.sha256()
-    for f in ("hobi_sweep.cu", "hobi_fastmath.cuh", "hobi_internal.cuh"):
-        with open(os.path.join(ROOT, "paper_1301_5914_b200", "csrc", f), "rb") as fh:
-            h.update(fh.read())
-    return h.hexdigest()
+
+def _sweep_source_hash(lib_path=None):
+    """SHA-256 of the main sweep kernel's SASS in the built library: stamps the
+    committed ncu traffic capture, which stays valid exactly as long as the
+    kernel's machine code is unchanged.  None if cuobjdump is unavailable."""
+    import hashlib
+    import re
+    import shutil
+    import subprocess
+
+    lib_path = lib_path or os.path.join(ROOT, "paper_1301_5914_b200", "libhobi.so")
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    try:
+        dump = subprocess.run([tool, "-sass", lib_path], capture_output=True, text=True, timeout=300).stdout
+    except Exception:  # noqa: BLE001
+        return None
+    for block in dump.split("Function : ")[1:]:
+        name, _, body = block.partition("\n")
+        if MAIN_SWEEP not in name:
+            continue
+        lines = []
+        for ln in body.splitlines():
+            t = ln.strip()
+            if t.startswith("....") or t.startswith("Fatbin"):
+                break
+            if t:
+                lines.append(re.sub(r"\s+", " ", t))
+        return hashlib.sha256("\n".join(lines).encode()).hexdigest()
+    return None
 
 
 def _committed_traffic(config, world):
@@ -390,8 +413,11 @@ def _committed_traffic(config, world):
         t = json.load(open(tfile))
     except Exception:  # noqa: BLE001
         return None, "no committed ncu capture"
-    if t.get("sweep_source_sha256") != _sweep_source_hash():
-        return None, "committed ncu capture is stale (sweep sources changed since)"
+    stamp = _sweep_source_hash()
+    if stamp is None:
+        return None, "cannot read the sweep kernel's SASS (cuobjdump unavailable)"
+    if t.get("sweep_sass_sha256") != stamp:
+        return None, "committed ncu capture is stale (the sweep kernel's SASS changed since)"
     if t.get("config") != config or t.get("n_gpus", 1) != world:
         return None, f"committed ncu capture is for config {t.get('config')} on {t.get('n_gpus', 1)} GPU(s)"
     return t["bytes_per_launch"], t.get("source")
@@ -634,7 +660,7 @@ def run_ours(a):
     peak_total = float(sum(p for part in peak_all for p in part))
     # whole-job sweep rate: every GPU's pairs over the slowest GPU's sweep time
     achieved = pairs_step * FLOPS_PER_PAIR / (worst["sweep_ms"] * 1e-3) * 1e-12
-    launches_total = int(max_over_ranks(float(launches_total)))
+    launches_total = int(sum(run.gather_all(launches_total)))  # every GPU's kernels
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": a.steps,

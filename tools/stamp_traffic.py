@@ -1,6 +1,7 @@
 """Write profiles/sweep_traffic.json from an `ncu --set full` capture of the
-main sweep launch, stamped with the SHA-256 of the sweep sources so bench.py
-reports it only while the kernel is unchanged.
+main sweep launch, stamped with the SHA-256 of the main sweep kernel's SASS in
+the built library, so bench.py reports it only while that machine code is
+unchanged.
 
     python tools/stamp_traffic.py gpurun_out/r2_sweep.ncu-rep 4 1 "<how it was captured>"
 """
@@ -29,7 +30,7 @@ wr = float(main["dram__bytes_write.sum"]) * scale[units["dram__bytes_write.sum"]
 doc = {
     "config": config, "n_gpus": ngpu,
     "kernel": main["Kernel Name"].split("(")[0],
-    "sweep_source_sha256": bench._sweep_source_hash(),
+    "sweep_sass_sha256": bench._sweep_source_hash(),
     "bytes_per_launch": rd + wr, "dram_bytes_read": rd, "dram_bytes_write": wr,
     "duration_ms": float(main["gpu__time_duration.sum"]),
     "fp64_pipe_active_pct": float(main["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]),
