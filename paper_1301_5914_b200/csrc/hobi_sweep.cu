@@ -683,14 +683,23 @@ int launch_sweep(hobi_ctx* c, const double* tgt, int64_t ldt, int64_t t0, int64_
         if (rem_n < rem_w && rem_w * 20 > rows) vi = narrow;
       }
       // small problems: if the tuned tile leaves too few work items for 148
-      // SMs, use 128-row tiles (same sums bitwise, more parallelism)
+      // SMs, use 128-row tiles (same sums bitwise, more parallelism) -- unless
+      // the wide tile, run as one launch with a part-filled last tile, still
+      // gives every CTA slot two items: then the wide tile's cheaper pairs win
+      // (config 2: 0.182 vs 0.197 ms per sweep; config 1 keeps the 128-row
+      // tile, 0.033 vs 0.052 ms; profiles/r02_small_configs.md)
       const int64_t items = (int64_t)nblk(t1 - t0, kSweepThreads * tab[vi].r) * n_groups;
-      if (!pinned && items < 8 * 296) vi = small;
+      const int64_t wide_items = (int64_t)nblk(t1 - t0, kSweepThreads * tab[wide].r) * n_groups;
+      bool single = false;
+      if (!pinned && items < 8 * 296) {
+        single = wide_items >= 2 * 296;
+        vi = single ? wide : small;
+      }
       seg[0].fn = tab[vi].fn;
       seg[0].r = tab[vi].r;
       const int64_t tile = (int64_t)kSweepThreads * seg[0].r;
       const int64_t whole = (t1 - t0) / tile * tile;
-      if (!pinned && seg[0].r > 1 && whole > 0 && whole < t1 - t0) {
+      if (!pinned && !single && seg[0].r > 1 && whole > 0 && whole < t1 - t0) {
         seg[0].b = t0 + whole;
         seg[1] = {tab[small].fn, tab[small].r, t0 + whole, t1};
         nseg = 2;

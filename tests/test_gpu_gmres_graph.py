@@ -31,8 +31,9 @@ for name in ("c1", "c2", "star_l2", "star_l3", "uv_sphere", "star_l2_lobi"):
     scheme = str(g["scheme"]) if "scheme" in g else "hobi"
     cases.append((name, FlatMesh(g["vertices"], g["normals"], g["faces"]), PhysicalParams(*g["params"]),
                   ChargeSystem(g["qpos"], g["q"]), int(g["restart"]), scheme))
-c3 = baseline_config(3)  # n = 20484: the single-CTA MGS; restart 20
-cases.append(("c3", c3.mesh, PhysicalParams(c3.eps1, c3.eps2, c3.kappa), c3.charges, c3.restart, "hobi"))
+for idx in (3, 4):  # n = 20484: the single-CTA MGS; n = 81924: the cooperative MGS inside the graph
+    cf = baseline_config(idx)
+    cases.append((f"c{idx}", cf.mesh, PhysicalParams(cf.eps1, cf.eps2, cf.kappa), cf.charges, cf.restart, "hobi"))
 for name, mesh, params, charges, restart, scheme in cases:
     cfg = SolverConfig(workers=1, restart=restart, scheme=scheme)
     prob = discretize(mesh, params, charges, cfg)
@@ -65,7 +66,7 @@ def test_graph_cycles_bitwise_equal_host_loop(tmp_path):
     for name in [k for k in g if not k.endswith("_meta")]:
         assert np.array_equal(g[name], h[name]), name
         assert np.array_equal(g[name + "_meta"], h[name + "_meta"]), name
-        if name != "c3":
-            ref = golden(name)
+        if name != "c4":  # config 3: the pbbem solve fixture (tests/golden/c3_solve.npz)
+            ref = golden("c3_solve" if name == "c3" else name)
             assert int(g[name + "_meta"][0]) == int(ref["iterations"]), name
             assert int(g[name + "_meta"][1]) == int(ref["matvecs"]), name

@@ -1,3 +1,5 @@
 set -x
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 4 -c 3 -o gpurun_out/r2_sweep_b python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-solve > gpurun_out/r2_ncu_full_b.log 2>&1
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r2_tall4.log 2>&1
+timeout 300 python tools/solve_table.py 1 2 3 4 > gpurun_out/r2_solve_table4.jsonl 2>&1
+timeout 300 python tools/size_sweep.py > gpurun_out/r2_size_sweep2.txt 2>&1
+timeout 600 python tools/split_model.py > gpurun_out/r2_split_model.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r2_tall5.log 2>&1
