@@ -57,9 +57,9 @@ def _rows_task(args):
     return rs._apply_range(_PROB, u, lo, lo + ROWS)
 
 
-def _problem(cfg, workers):
+def _problem(cfg, workers, scheme="hobi"):
     params = rk.PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa)
-    scfg = rs.SolverConfig(scheme="hobi", workers=workers, restart=cfg.restart, tolerance=cfg.tol)
+    scfg = rs.SolverConfig(scheme=scheme, workers=workers, restart=cfg.restart, tolerance=cfg.tol)
     t0 = time.time()
     prob = rs.discretize(RMesh(vertices=cfg.mesh.vertices, normals=cfg.mesh.normals, faces=cfg.mesh.faces),
                          params, RCharges(positions=cfg.charges.positions, charges=cfg.charges.charges), scfg)
@@ -67,14 +67,14 @@ def _problem(cfg, workers):
     return prob, scfg
 
 
-def rows_case(index, workers=5):
+def rows_case(index, workers=5, scheme="hobi"):
     global _PROB
     t0 = time.time()
     cfg = baseline_config(index)
-    nv = cfg.mesh.n_vertices
-    print(f"c{index}rows: N_v={nv} N_f={cfg.mesh.n_faces}", flush=True)
-    prob, _ = _problem(cfg, 1)
+    print(f"c{index}rows ({scheme}): N_v={cfg.mesh.n_vertices} N_f={cfg.mesh.n_faces}", flush=True)
+    prob, _ = _problem(cfg, 1, scheme)
     _PROB = prob
+    nv = prob.n_collocation  # N_v for hobi, N_f for lobi
     u = np.random.default_rng(0).standard_normal(2 * nv)
     starts = row_blocks(nv)
     with mp.get_context("fork").Pool(min(workers, len(starts))) as pool:
@@ -85,10 +85,11 @@ def rows_case(index, workers=5):
                rows=idx, Au_phi=np.concatenate([p[0] for p in parts]),
                Au_dphi=np.concatenate([p[1] for p in parts]),
                rhs_phi=s1 / cfg.eps1, rhs_dphi=s2 / cfg.eps1,
-               params=np.array([cfg.eps1, cfg.eps2, cfg.kappa]),
+               params=np.array([cfg.eps1, cfg.eps2, cfg.kappa]), scheme=np.array(scheme),
                generated_by=np.array("pbbem solver._apply_range + kernels.source_terms_at"))
-    np.savez_compressed(os.path.join(HERE, f"c{index}_rows.npz"), **out)
-    print(f"c{index}rows: {time.time() - t0:.0f} s", flush=True)
+    tag = "" if scheme == "hobi" else "_" + scheme
+    np.savez_compressed(os.path.join(HERE, f"c{index}_rows{tag}.npz"), **out)
+    print(f"c{index}rows ({scheme}): {time.time() - t0:.0f} s", flush=True)
 
 
 def solve_case(index, workers=8, name=None):
@@ -130,6 +131,7 @@ def solve_case(index, workers=8, name=None):
 
 def main():
     jobs = {"c3": lambda: solve_case(3), "c4rows": lambda: rows_case(4), "c5rows": lambda: rows_case(5),
+            "c4lobirows": lambda: rows_case(4, scheme="lobi"),
             "c4solve": lambda: solve_case(4, workers=int(os.environ.get("WORKERS", "6")))}
     for name in sys.argv[1:] or ["c3", "c4rows", "c5rows"]:
         jobs[name]()

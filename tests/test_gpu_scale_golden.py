@@ -1,6 +1,7 @@
 """Parity at the BASELINE sizes against the reference itself.
 
-The fixtures (tests/golden/c3_solve.npz, c4_rows.npz, c5_rows.npz, made by
+The fixtures (tests/golden/c3_solve.npz, c4_rows.npz, c5_rows.npz,
+c4_rows_lobi.npz (the LOBI scheme), made by
 tests/golden/make_scale_golden.py running unmodified pbbem in the build
 container) hold reference outputs for the seeded configs 3, 4 (the bench
 config) and 5; the meshes are regenerated here and checked against the
@@ -29,7 +30,7 @@ def _fixture(name):
     return dict(np.load(path))
 
 
-def _problem(index, fx):
+def _problem(index, fx, scheme="hobi"):
     from scale_hash import input_hash
 
     from paper_1301_5914_b200 import PhysicalParams, SolverConfig, discretize
@@ -38,19 +39,20 @@ def _problem(index, fx):
     cfg = baseline_config(index)
     assert input_hash(cfg) == str(fx["input_sha256"]), "generated mesh/charges differ from the fixture's"
     assert np.array_equal(fx["params"], [cfg.eps1, cfg.eps2, cfg.kappa])
-    scfg = SolverConfig(workers=1, restart=cfg.restart, tolerance=cfg.tol)
+    scfg = SolverConfig(workers=1, restart=cfg.restart, tolerance=cfg.tol, scheme=scheme)
     return cfg, scfg, discretize(cfg.mesh, PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa), cfg.charges, scfg)
 
 
-@pytest.mark.parametrize("index", [4, 5])
-def test_rows_match_reference_at_scale(index):
-    from paper_1301_5914_b200 import assemble_rhs, matvec_hobi
+@pytest.mark.parametrize("index,scheme", [(4, "hobi"), (5, "hobi"), (4, "lobi")])
+def test_rows_match_reference_at_scale(index, scheme):
+    from paper_1301_5914_b200 import assemble_rhs, matvec_hobi, matvec_lobi
 
-    fx = _fixture(f"c{index}_rows")
-    cfg, _, prob = _problem(index, fx)
-    nv = prob.n_collocation
+    fx = _fixture(f"c{index}_rows" + ("" if scheme == "hobi" else "_" + scheme))
+    assert str(fx.get("scheme", "hobi")) == scheme
+    cfg, _, prob = _problem(index, fx, scheme)
+    nv = prob.n_collocation  # N_v (hobi) or N_f (lobi)
     u = np.random.default_rng(int(fx["u_seed"])).standard_normal(2 * nv)
-    au = matvec_hobi(prob, u)
+    au = (matvec_hobi if scheme == "hobi" else matvec_lobi)(prob, u)
     rows = fx["rows"]
     worst = 0.0
     for blk in range(0, rows.size, 24):
