@@ -261,9 +261,10 @@ int hobi_timing(hobi_ctx* ctx, double* sweep_ms, int64_t* sweep_launches, int64_
 /* Tuning hook: select all-pairs sweep variant `variant` (< 0 keeps the
  * current one); reports the number of variants and the active one's name.
  * A selected variant is pinned: it runs every row range as is.  Unpinned
- * (default), the 768-row tile falls back to 512-row tiles for ranges that
+ * (default), the 896-row tile falls back to 512-row tiles for ranges that
  * leave fewer rows past the last whole tile that way, and to 128-row
- * tiles when a range has too few work items; all variants and fallbacks
+ * tiles (or one wide-tile launch with a part-filled last tile) when a range
+ * has too few work items; all variants and fallbacks
  * produce bitwise identical results (the environment variable
  * HOBI_SWEEP_VARIANT sets the unpinned default at context creation). */
 int hobi_sweep_variant(hobi_ctx* ctx, int variant, int* count, char* name, int name_len);

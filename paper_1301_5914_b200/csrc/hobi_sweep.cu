@@ -23,8 +23,8 @@
 // K1/K2-only energy sweep), SELF (LOBI self-pair mask, applied only on source
 // tiles that overlap the item's rows), R targets per thread, MINB CTAs per SM,
 // UNROLL of the source loop, STEP (step-major pair arithmetic).  launch_sweep
-// picks a 768-row or a 512-row tile (whichever leaves fewer rows past the last
-// whole tile), falls back to 128-row tiles for small ranges, and runs the rows past the
+// picks an 896-row or a 512-row tile (whichever leaves fewer rows past the last
+// whole tile; small ranges: 128-row tiles, or one wide launch), and runs the rows past the
 // last whole tile as a second 128-row-tile launch on a second side stream.
 #include <algorithm>
 #include <cmath>
