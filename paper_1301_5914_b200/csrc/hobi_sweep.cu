@@ -566,7 +566,8 @@ static const SweepVariant kVariants[] = {
     HOBI_V(4, 4, 1), HOBI_V(3, 4, 1), HOBI_V(6, 2, 1), HOBI_V(8, 2, 1), HOBI_V(3, 4, 2),
     HOBI_V(4, 4, 2), HOBI_V(5, 3, 1), HOBI_VS(6, 2, 1), HOBI_VS(4, 3, 1), HOBI_VS(3, 4, 1),
     HOBI_VS(4, 3, 2), HOBI_VS(4, 3, 4), HOBI_VS(6, 2, 2), HOBI_VS(3, 4, 2), HOBI_VS(5, 3, 2),
-    HOBI_VS(8, 2, 2), HOBI_VS(6, 2, 3), HOBI_VS(7, 2, 3),
+    HOBI_VS(8, 2, 2), HOBI_VS(6, 2, 3), HOBI_VS(7, 2, 3), HOBI_V(1, 8, 4), HOBI_V(1, 8, 8),
+    HOBI_V(1, 6, 4),
 };
 #undef HOBI_V
 #undef HOBI_VS
@@ -600,10 +601,14 @@ static const SweepVariant kLaplaceSelfVariants[] = {
     {sweep_kernel<kLaplace, true, true, 4, 3, 2>, 4, "laplace_self_R4_minb3_unroll2"},
     {sweep_kernel<kLaplace, true, true, 1, 6, 2>, 1, "laplace_self_R1_minb6_unroll2"},
 };
-constexpr int kSmallVariant = 3;   // R1_minb8_unroll2
+// R1_minb8_unroll4: 128-row tiles with four sources in flight per thread
+// (config 1: 0.032 vs 0.039 ms for unroll 2, config 2: 0.192 vs 0.197 ms,
+// profiles/r02_small_configs.md)
+constexpr int kSmallVariant = 23;
 constexpr int kWideVariant = 22;   // step_R7_minb2_unroll3: 896-row tiles, the default
 constexpr int kNarrowVariant = 15; // step_R4_minb3_unroll2: 512-row tiles
-static_assert(kWideVariant < kNumVariants && kNarrowVariant < kNumVariants, "variant table");
+static_assert(kWideVariant < kNumVariants && kNarrowVariant < kNumVariants && kSmallVariant < kNumVariants,
+              "variant table");
 
 // Physics folded into the per-source record and two launch constants (see
 // hobi_fastmath.cuh).  Screened: with Ap = er/k, Bp = (er-1)/k the wp-weighted
