@@ -33,7 +33,7 @@ for name in ("c1", "c2", "star_l2", "star_l3", "uv_sphere", "star_l2_lobi"):
                   ChargeSystem(g["qpos"], g["q"]), int(g["restart"]), scheme))
 for idx in (3, 4):  # n = 20484: the single-CTA MGS; n = 81924: the cooperative MGS inside the graph
     cf = baseline_config(idx)
-    cases.append((f"c{idx}", cf.mesh, PhysicalParams(cf.eps1, cf.eps2, cf.kappa), cf.charges, cf.restart, "hobi"))
+    cases.append((f"c{{idx}}", cf.mesh, PhysicalParams(cf.eps1, cf.eps2, cf.kappa), cf.charges, cf.restart, "hobi"))
 for name, mesh, params, charges, restart, scheme in cases:
     cfg = SolverConfig(workers=1, restart=restart, scheme=scheme)
     prob = discretize(mesh, params, charges, cfg)
