@@ -176,6 +176,46 @@ struct GmresWorkspace {
   int m = -1, grid = 1;
 };
 
+// numpy's float64 add.reduce over a short contiguous row (n <= 128): a
+// left-to-right sum for n < 8, otherwise eight interleaved accumulators folded
+// as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail -- the order
+// `.sum(axis=1)` uses for the 4- and 16-point rows of solver.py:350-360.
+template <typename Term>
+__device__ __forceinline__ void numpy_row_sum(int n, Term term, double& s1, double& s2) {
+  if (n < 8) {
+    s1 = 0.0;
+    s2 = 0.0;
+    for (int m = 0; m < n; ++m) {
+      double t1, t2;
+      term(m, t1, t2);
+      s1 += t1;
+      s2 += t2;
+    }
+    return;
+  }
+  double r1[8], r2[8];
+  const int nb = n - n % 8;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) term(j, r1[j], r2[j]);
+  for (int i = 8; i < nb; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double t1, t2;
+      term(i + j, t1, t2);
+      r1[j] += t1;
+      r2[j] += t2;
+    }
+  }
+  s1 = ((r1[0] + r1[1]) + (r1[2] + r1[3])) + ((r1[4] + r1[5]) + (r1[6] + r1[7]));
+  s2 = ((r2[0] + r2[1]) + (r2[2] + r2[3])) + ((r2[4] + r2[5]) + (r2[6] + r2[7]));
+  for (int m = nb; m < n; ++m) {
+    double t1, t2;
+    term(m, t1, t2);
+    s1 += t1;
+    s2 += t2;
+  }
+}
+
 struct ChargeWorkspace {  // energy / RHS buffers for one charge set size
   int64_t nc = -1;
   DevBuf<double> q, qpos, tq, part, v, recv, e;
@@ -240,6 +280,7 @@ struct hobi_ctx {
   std::vector<cudaEvent_t> ev_pool;   // recorded sweep brackets, read lazily
   // launch bookkeeping cached per sweep instantiation: (kernel, CTAs per SM)
   std::vector<std::pair<const void*, int>> occupancy;
+  bool singular_smem_set = false;  // singular_fast_kernel's dynamic shared-memory opt-in on this device
   int sms = 0;
   size_t ev_used = 0;                  // pairs of ev_pool in flight
   double sweep_ms = 0.0;
@@ -279,6 +320,7 @@ int kernel_values_device(const double* d, const double* nx, const double* ny, in
 
 // Duffy swap over pairs [p0, p1) on `stream` (hobi_literal.cu)
 int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1, cudaStream_t stream);
+int launch_singular_fast(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1, cudaStream_t stream);
 
 // GMRES (hobi_gmres.cu)
 struct DeviceOperator {

@@ -1,9 +1,12 @@
 // Low-volume kernels written as literal transcriptions of the reference
 // arithmetic (compiled with -fmad=false, libdevice exp/expm1/sqrt, IEEE
-// division): the Duffy singular swap, the charge source terms
-// (K-E) and the kernel-value test hook.  These touch O(N) pairs, so fidelity
-// to kernels.py beats instruction count here.
+// division): the charge source terms (K-E), the kernel-value test hook and
+// the literal forms of the Duffy singular swap --
+// HOBI_SINGULAR=warp|serial, the check the default singular_fast_kernel
+// (hobi_sweep.cu) is tested against.  These touch O(N) pairs, so fidelity to
+// kernels.py beats instruction count here.
 #include <cstdlib>
+#include <cstring>
 
 #include "hobi_internal.cuh"
 
@@ -54,46 +57,6 @@ __global__ void kernel_values_kernel(const double* __restrict__ d, const double*
 __device__ __forceinline__ double interp3(const double* __restrict__ u, int i0, int i1, int i2,
                                           const double* __restrict__ b) {
   return u[i0] * b[0] + u[i1] * b[1] + u[i2] * b[2];  // _interp, solver.py:269-275
-}
-
-// numpy's float64 add.reduce over a short contiguous row (n <= 128): a
-// left-to-right sum for n < 8, otherwise eight interleaved accumulators folded
-// as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail -- the order
-// `.sum(axis=1)` uses for the 4- and 16-point rows of solver.py:350-360.
-template <typename Term>
-__device__ __forceinline__ void numpy_row_sum(int n, Term term, double& s1, double& s2) {
-  if (n < 8) {
-    s1 = 0.0;
-    s2 = 0.0;
-    for (int m = 0; m < n; ++m) {
-      double t1, t2;
-      term(m, t1, t2);
-      s1 += t1;
-      s2 += t2;
-    }
-    return;
-  }
-  double r1[8], r2[8];
-  const int nb = n - n % 8;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) term(j, r1[j], r2[j]);
-  for (int i = 8; i < nb; i += 8) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      double t1, t2;
-      term(i + j, t1, t2);
-      r1[j] += t1;
-      r2[j] += t2;
-    }
-  }
-  s1 = ((r1[0] + r1[1]) + (r1[2] + r1[3])) + ((r1[4] + r1[5]) + (r1[6] + r1[7]));
-  s2 = ((r2[0] + r2[1]) + (r2[2] + r2[3])) + ((r2[4] + r2[5]) + (r2[6] + r2[7]));
-  for (int m = nb; m < n; ++m) {
-    double t1, t2;
-    term(m, t1, t2);
-    s1 += t1;
-    s2 += t2;
-  }
 }
 
 // One incident pair p: Duffy sum on the rotated element minus the regular-rule
@@ -147,7 +110,7 @@ __global__ void singular_kernel(int64_t p0, int64_t p1, const int* __restrict__ 
 // land in shared memory, and lanes 0 and 1 sum the regular and the Duffy row
 // in numpy's order (numpy_row_sum) -- the identical operations in the
 // identical order as singular_kernel, so the output is bitwise the same, with
-// 20 evaluations in parallel instead of in series (HOBI_SINGULAR_SERIAL=1
+// 20 evaluations in parallel instead of in series (HOBI_SINGULAR=serial
 // selects the serial kernel, for the bitwise regression test).
 constexpr int kSingWarps = 4;          // pairs per 128-thread block
 constexpr int kSingMaxTerms = 16 + 64;  // nq <= 16, nd <= 64 (hobi_create)
@@ -264,11 +227,21 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1, cudaStream_t stream) {
   if (p1 <= p0) return 0;
-  static const bool serial = [] {
-    const char* e = getenv("HOBI_SINGULAR_SERIAL");
-    return e && e[0] == '1';
+  // HOBI_SINGULAR: "fast" (default, hobi_sweep.cu), "warp" (literal
+  // transcription, one warp per pair) or "serial" (literal, one thread per
+  // pair; HOBI_SINGULAR_SERIAL=1 is the older spelling)
+  static const int kind = [] {
+    const char* s = getenv("HOBI_SINGULAR_SERIAL");
+    if (s && s[0] == '1') return 2;
+    const char* e = getenv("HOBI_SINGULAR");
+    if (e && !strcmp(e, "serial")) return 2;
+    if (e && !strcmp(e, "warp")) return 1;
+    return 0;
   }();
-  if (serial)
+  if (kind == 0) {
+    int rc = launch_singular_fast(c, u_dev, p0, p1, stream);
+    if (rc) return rc;
+  } else if (kind == 2)
     singular_kernel<<<nblk(p1 - p0, 128), 128, 0, stream>>>(
         p0, p1, c->pair_vertex.p, c->pair_face.p, c->pair_gverts.p, c->faces.p, c->vert.p, c->vnrm.p,
         c->reg_pos.p, c->reg_nrm.p, c->reg_w.p, c->reg_bary.p, c->nq, c->duf_pos.p, c->duf_nrm.p,

@@ -1,7 +1,14 @@
-"""The warp-per-pair Duffy swap (singular_warp_kernel) against the serial
-one-thread-per-pair kernel it replaced: identical operations in identical
-order, so matvecs must agree bit for bit -- on the default 4 + 16-point rules
-and on a 6x6 Duffy rule (4 + 36 terms: lanes loop past 32)."""
+"""The three Duffy-swap kernels (solver.py:336-363).
+
+* warp-per-pair literal kernel (singular_warp_kernel, HOBI_SINGULAR=warp)
+  against the serial one-thread-per-pair literal kernel: identical operations
+  in identical order, so matvecs agree bit for bit;
+* the default thread-per-term kernel (singular_fast_kernel: the sweep's
+  rsqrt/expm1 arithmetic, numpy's summation order) against the literal one:
+  the matvec within 1e-14 relative (L2) and the reference goldens within 1e-12.
+
+Default 4 + 16-point rules, and a 6x6 Duffy rule (4 + 36 terms: the warp
+kernel's lanes loop past 32, the fast kernel packs 6 pairs per block)."""
 
 import os
 import subprocess
@@ -30,12 +37,14 @@ np.savez(sys.argv[1], **out)
 """
 
 
-def _run(tmp_path, serial):
-    path = os.path.join(tmp_path, f"mv_{int(serial)}.npz")
+def _run(tmp_path, kind, variant=None):
+    path = os.path.join(tmp_path, f"mv_{kind}_{variant}.npz")
     env = dict(os.environ, PYTHONPATH=ROOT)
     env.pop("HOBI_SINGULAR_SERIAL", None)
-    if serial:
-        env["HOBI_SINGULAR_SERIAL"] = "1"
+    env.pop("HOBI_SINGULAR_VARIANT", None)
+    env["HOBI_SINGULAR"] = kind
+    if variant is not None:
+        env["HOBI_SINGULAR_VARIANT"] = str(variant)
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT), path], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
@@ -43,9 +52,30 @@ def _run(tmp_path, serial):
 
 
 def test_warp_singular_kernel_bitwise_equals_serial(tmp_path):
-    warp = _run(tmp_path, False)
-    serial = _run(tmp_path, True)
+    warp = _run(tmp_path, "warp")
+    serial = _run(tmp_path, "serial")
     for name in warp:
         assert np.array_equal(warp[name], serial[name]), name
         g = golden(name)
         assert np.linalg.norm(warp[name] - g["Au"]) <= 1e-12 * np.linalg.norm(g["Au"]), name
+
+
+def test_fast_singular_kernel_matches_literal(tmp_path):
+    fast = _run(tmp_path, "fast")
+    warp = _run(tmp_path, "warp")
+    for name in fast:
+        rel = np.linalg.norm(fast[name] - warp[name]) / np.linalg.norm(warp[name])
+        assert rel <= 1e-14, (name, rel)
+        g = golden(name)
+        assert np.linalg.norm(fast[name] - g["Au"]) <= 1e-12 * np.linalg.norm(g["Au"]), name
+
+
+def test_fast_singular_tilings_bitwise_identical(tmp_path):
+    """Every block tiling of the default-rule kernel (HOBI_SINGULAR_VARIANT
+    1-5: pairs per block, registers) does the same operations per term and
+    the same row sums: bitwise equal matvecs."""
+    base = _run(tmp_path, "fast", 1)
+    for v in (2, 3, 4, 5):
+        other = _run(tmp_path, "fast", v)
+        for name in base:
+            assert np.array_equal(base[name], other[name]), (v, name)

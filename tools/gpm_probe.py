@@ -58,6 +58,21 @@ def main():
     print("gpm supported:", sup.isSupportedDevice)
     bus = nv.nvmlDeviceGetMemoryBusWidth(h)
     mclk = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_MEM)
+    for attempt in ("before CUDA init", "streaming on"):
+        if attempt == "streaming on":
+            try:
+                nv.nvmlGpmSetStreamingEnabled(h, 1)
+            except nv.NVMLError as e:
+                print("set streaming:", e)
+        try:
+            a = nv.nvmlGpmSampleAlloc()
+            nv.nvmlGpmSampleGet(h, a)
+            time.sleep(0.2)
+            b = nv.nvmlGpmSampleAlloc()
+            nv.nvmlGpmSampleGet(h, b)
+            print(attempt, "ok", metrics(h, a, b))
+        except nv.NVMLError as e:
+            print(attempt, "failed:", e)
     print("bus width", bus, "mem max MHz", mclk, "=> DDR peak GB/s", 2 * mclk * 1e6 * bus / 8 / 1e9)
 
     from paper_1301_5914_b200 import PhysicalParams, SolverConfig, discretize
