@@ -184,6 +184,7 @@ static int alloc_operands(hobi_ctx* c) {
   int rc;
   if (c->nt > 0 && (rc = prepare_targets(c))) return rc;
   if ((rc = prepare_static_sources(c))) return rc;
+  if ((rc = prepare_singular(c))) return rc;
   HOBI_CUDA(cudaStreamSynchronize(c->stream));
   return 0;
 }

@@ -250,6 +250,9 @@ struct hobi_ctx {
   hobi::DevBuf<double> duf_pos, duf_nrm, duf_w;  // pair order (3nf,nd,3)...
   hobi::DevBuf<double> node0_pos, node0_nrm;     // rotation-0 curved nodes (nf,10,3)
   hobi::DevBuf<int> pair_vertex, pair_face, pair_gverts, pair_starts;
+  // per incident pair, 8 ints: vertex, face, the face's vertices, the rotated
+  // element's vertices (prepare_singular; one 32-byte read per pair)
+  hobi::DevBuf<int> pair_rec;
   std::vector<int> h_pair_starts;
   hobi::DevBuf<double> reg_bary, duf_bary;   // (nq,3), (nd,3)
   hobi::DevBuf<double> lobi_area;            // (nf)
@@ -280,7 +283,7 @@ struct hobi_ctx {
   std::vector<cudaEvent_t> ev_pool;   // recorded sweep brackets, read lazily
   // launch bookkeeping cached per sweep instantiation: (kernel, CTAs per SM)
   std::vector<std::pair<const void*, int>> occupancy;
-  bool singular_smem_set = false;  // singular_fast_kernel's dynamic shared-memory opt-in on this device
+  bool singular_smem_set = false;  // singular_fast_kernel's shared-memory opt-in on this device
   int sms = 0;
   size_t ev_used = 0;                  // pairs of ev_pool in flight
   double sweep_ms = 0.0;
@@ -309,6 +312,7 @@ int sweep_variant_count();
 const char* sweep_variant_name(int v);
 int prepare_targets(hobi_ctx* c);
 int prepare_static_sources(hobi_ctx* c);
+int prepare_singular(hobi_ctx* c);
 int matvec_rows_device(hobi_ctx* c, const double* u_dev, int64_t lo, int64_t hi, double* o1,
                        double* o2);
 int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev);

@@ -72,10 +72,10 @@ def test_fast_singular_kernel_matches_literal(tmp_path):
 
 def test_fast_singular_tilings_bitwise_identical(tmp_path):
     """Every block tiling of the default-rule kernel (HOBI_SINGULAR_VARIANT
-    1-5: pairs per block, registers) does the same operations per term and
-    the same row sums: bitwise equal matvecs."""
-    base = _run(tmp_path, "fast", 1)
-    for v in (2, 3, 4, 5):
+    1-8: pairs and threads per block, registers; the default is 4) does the
+    same operations per term and the same row sums: bitwise equal matvecs."""
+    base = _run(tmp_path, "fast")
+    for v in range(1, 9):
         other = _run(tmp_path, "fast", v)
         for name in base:
             assert np.array_equal(base[name], other[name]), (v, name)
