@@ -24,6 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 UNITS = {
     "hobi_api.cu": [],
     "hobi_sweep.cu": [],
+    "hobi_singular.cu": [],
     "hobi_gmres.cu": [],
     "hobi_group.cu": [],
     "hobi_msms.cu": [],
@@ -31,7 +32,7 @@ UNITS = {
     "hobi_literal.cu": ["-fmad=false"],
     "hobi_kirkwood.cu": ["-fmad=false"],
 }
-HEADERS = ["hobi_internal.cuh", "hobi_fastmath.cuh", "hobi_default_rules.inc"]
+HEADERS = ["hobi_internal.cuh", "hobi_fastmath.cuh", "hobi_tma.cuh", "hobi_default_rules.inc"]
 
 
 def _nvcc():

@@ -283,7 +283,7 @@ struct hobi_ctx {
   std::vector<cudaEvent_t> ev_pool;   // recorded sweep brackets, read lazily
   // launch bookkeeping cached per sweep instantiation: (kernel, CTAs per SM)
   std::vector<std::pair<const void*, int>> occupancy;
-  bool singular_smem_set = false;  // singular_fast_kernel's shared-memory opt-in on this device
+  const double* singular_etab = nullptr;  // exp table on this device; set once singular_fast_kernel is opted in
   int sms = 0;
   size_t ev_used = 0;                  // pairs of ev_pool in flight
   double sweep_ms = 0.0;
@@ -305,6 +305,7 @@ int build_geometry(hobi_ctx* c, const int* pair_of_slot, int* first_bad_slot, in
 
 // sweep (hobi_sweep.cu)
 int upload_exp_table();
+const double* exp_table_device();
 int collect_sweep_timing(hobi_ctx* c);
 int charge_workspace(hobi_ctx* c, int64_t nc);
 std::vector<int2> make_groups(int n_src_tiles, int64_t target_tiles_at_8);

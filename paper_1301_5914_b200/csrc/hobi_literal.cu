@@ -3,7 +3,7 @@
 // division): the charge source terms (K-E), the kernel-value test hook and
 // the literal forms of the Duffy singular swap --
 // HOBI_SINGULAR=warp|serial, the check the default singular_fast_kernel
-// (hobi_sweep.cu) is tested against.  These touch O(N) pairs, so fidelity to
+// (hobi_singular.cu) is tested against.  These touch O(N) pairs, so fidelity to
 // kernels.py beats instruction count here.
 #include <cstdlib>
 #include <cstring>

@@ -1,9 +1,5 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_singular.py -q -x > gpurun_out/r2m_singular.txt 2>&1
-for c in 1 4; do
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:singular --csv --log-file gpurun_out/r2m_launch_c$c.csv python tools/launch_breakdown.py $c > /dev/null 2>&1
-  python tools/launch_summary.py gpurun_out/r2m_launch_c$c.csv > gpurun_out/r2m_launch_summary_c$c.txt 2>&1
-done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:singular_fast -s 2 -c 1 -o gpurun_out/r2m_singular_c4 python tools/launch_breakdown.py 4 > gpurun_out/r2m_ncu_full.log 2>&1
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2m_gputest.txt 2>&1; echo "gputest rc=$?" >> gpurun_out/r2m_gputest.txt
-timeout 600 python bench.py > gpurun_out/r2m_bench.json 2> gpurun_out/r2m_bench.err
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2n_gputest.txt 2>&1; echo "gputest rc=$?" >> gpurun_out/r2n_gputest.txt
+timeout 600 python bench.py > gpurun_out/r2n_bench.json 2> gpurun_out/r2n_bench.err
+HOBI_FORCE_NCCL=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r2n_torchrun_n1.json 2> gpurun_out/r2n_torchrun_n1.err
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2n_smoke.txt 2>&1
