@@ -1,5 +1,4 @@
 set -x
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2n_gputest.txt 2>&1; echo "gputest rc=$?" >> gpurun_out/r2n_gputest.txt
-timeout 600 python bench.py > gpurun_out/r2n_bench.json 2> gpurun_out/r2n_bench.err
-HOBI_FORCE_NCCL=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r2n_torchrun_n1.json 2> gpurun_out/r2n_torchrun_n1.err
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2n_smoke.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2o_launch_list_c4.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-solve > gpurun_out/r2o_ncu_bench.log 2>&1
+python tools/launch_summary.py gpurun_out/r2o_launch_list_c4.csv > gpurun_out/r2o_launch_summary_c4.txt 2>&1
+timeout 1200 python bench.py --config 5 --steps 5 --warmup 3 > gpurun_out/r2o_bench_c5.json 2> gpurun_out/r2o_bench_c5.err
