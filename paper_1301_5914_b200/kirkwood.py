@@ -6,12 +6,14 @@ harmonics inside, modified spherical Bessel functions k_n(kappa r) outside,
 matched by continuity of phi and eps dphi/dr at r = a.  Vectorised over
 charges and evaluation points (the reference loops over charges).
 
-Two backends: "gpu" (default) runs the O(N_points x N_c x n_terms) Legendre
-sums -- the surface traces (kirkwood.py:193-203) and the charge-charge energy
-(kirkwood.py:180-188) -- in sm_100a kernels (csrc/hobi_kirkwood.cu) behind
-the C ABI and raises without a device, like every other product path;
-"host" keeps the vectorised numpy restatement for CPU-only validation.  The
-O(N_c x n_terms) coefficients are computed on the host either way.
+The O(N_c x n_terms) coefficients (the Bessel log-derivative recurrence,
+the reaction coefficients, the trace rows) are computed here on the host, as
+the reference computes them (``kirkwood_coefficients``); the
+O(N_points x N_c x n_terms) Legendre sums -- the surface traces
+(kirkwood.py:193-203) and the charge-charge energy (kirkwood.py:180-188) --
+run in sm_100a kernels (csrc/hobi_kirkwood.cu) behind the C ABI and raise
+without a device, like every other product path.  The numpy form of those
+sums is test infrastructure, outside this package (tests/test_kirkwood.py).
 """
 
 from __future__ import annotations
@@ -46,18 +48,6 @@ class SphereProblem:
             if bad.size:
                 raise ValueError(f"charge {bad[0]} at distance {rho[bad[0]]} is not strictly "
                                  f"inside the sphere of radius {self.radius}")
-
-
-def legendre_table(nmax: int, x) -> np.ndarray:
-    """P_0..P_nmax(x) by the three-term recurrence; shape (nmax+1,) + x.shape."""
-    x = np.asarray(x, dtype=float)
-    out = np.empty((nmax + 1,) + x.shape)
-    out[0] = 1.0
-    if nmax >= 1:
-        out[1] = x
-    for n in range(1, nmax):
-        out[n + 1] = ((2 * n + 1) * x * out[n] - n * out[n - 1]) / (n + 1)
-    return out
 
 
 def bessel_log_derivative(nmax: int, x: float) -> np.ndarray:
@@ -133,15 +123,25 @@ def _gpu_energy(units, q, reac, rpow, nmax):
     return energy
 
 
-def kirkwood_series(problem: SphereProblem, n_terms: int = 40, backend: str = "gpu") -> KirkwoodSolution:
-    """Multipole solution for arbitrary interior charges (kirkwood.py:159-220).
+@dataclass(frozen=True)
+class KirkwoodCoefficients:
+    """Per-charge multipole data of kirkwood_series (kirkwood.py:159-178)."""
 
-    ``backend="gpu"`` evaluates the energy and the traces on the device
-    (no CPU fallback: raises without one); ``"host"`` uses numpy."""
+    nmax: int
+    rho: np.ndarray        # |y_k|
+    units: np.ndarray      # y_k / |y_k| (0 for a charge at the centre)
+    rpow: np.ndarray       # rho_k^n, (N_c, nmax+1)
+    reac: np.ndarray       # reaction-field coefficients, (N_c, nmax+1)
+    coef_phi: np.ndarray   # trace rows of phi, (N_c, nmax+1)
+    coef_dphi: np.ndarray  # trace rows of dphi/dn, (N_c, nmax+1)
+    tail_ratio: float
+
+
+def kirkwood_coefficients(problem: SphereProblem, n_terms: int = 40) -> KirkwoodCoefficients:
+    """The O(N_c x n_terms) part of kirkwood_series, on the host as the
+    reference computes it; the truncation check is its tail ratio."""
     if n_terms < 1:
         raise ValueError(f"n_terms must be >= 1, got {n_terms}")
-    if backend not in ("gpu", "host"):
-        raise ValueError(f"backend must be 'gpu' or 'host', got {backend!r}")
     nmax = n_terms - 1
     a, p = problem.radius, problem.params
     q = problem.charges.charges
@@ -155,45 +155,25 @@ def kirkwood_series(problem: SphereProblem, n_terms: int = 40, backend: str = "g
     reac = alpha * (a ** -(2 * n + 1.0) * (p.eps2 * ell + (n + 1) * p.eps1) / (n * p.eps1 - p.eps2 * ell))
     coef_phi = alpha * a ** -(n + 1.0) + reac * a**n
     coef_dphi = -(n + 1.0) * alpha * a ** -(n + 2.0) + n * reac * a ** (n - 1.0)
-    if backend == "gpu":
-        energy = _gpu_energy(units, q, reac, rpow, nmax)
-        energy *= FOUR_PI * KCAL_MOL_PER_E2_ANG
-        both = _gpu_traces(coef_phi, coef_dphi, units, rho, nmax)
-
-        def trace_gpu(which):
-            return lambda points: both(points)[which]
-
-        phi_fn, dphi_fn = trace_gpu(0), trace_gpu(1)
-    else:
-        # E = 1/2 sum_j q_j phi_reac(y_j): P_n(u_j . u_k) for all charge pairs at once
-        pn = legendre_table(nmax, np.clip(units @ units.T, -1.0, 1.0)) if len(q) else np.zeros((nmax + 1, 0, 0))
-        energy = 0.0
-        for j in range(len(q)):
-            energy += 0.5 * q[j] * float((reac * rpow[j][None, :] * pn[:, :, j].T).sum())
-        energy *= FOUR_PI * KCAL_MOL_PER_E2_ANG
-
-    def trace(coef):
-        def evaluate(points):
-            pts = np.asarray(points, dtype=float)
-            single = pts.ndim == 1
-            pts = pts.reshape(-1, 3)
-            _, rad = _directions(pts)
-            cos = rad @ units.T  # (m, nc)
-            cos[:, rho == 0.0] = 1.0
-            out = np.einsum("kn,nmk->m", coef, legendre_table(nmax, cos))
-            return out[0] if single else out
-
-        return evaluate
-
     if nmax >= 1 and len(q):
         last, prev = np.abs(coef_phi[:, nmax]), np.abs(coef_phi[:, nmax - 1])
         tail = float(np.where(last > 0.0, last / np.maximum(prev, 1e-300), 0.0).max())
     else:
         tail = 1.0 if np.abs(coef_phi).max(initial=0.0) > 0.0 else 0.0
-    if backend == "host":
-        phi_fn, dphi_fn = trace(coef_phi), trace(coef_dphi)
-    return KirkwoodSolution(energy=energy, phi=phi_fn, dphi_dn=dphi_fn,
-                            tail_ratio=tail, converged=tail <= 0.99, n_terms=n_terms)
+    return KirkwoodCoefficients(nmax, rho, units, rpow, reac, coef_phi, coef_dphi, tail)
+
+
+def kirkwood_series(problem: SphereProblem, n_terms: int = 40) -> KirkwoodSolution:
+    """Multipole solution for arbitrary interior charges (kirkwood.py:159-220):
+    coefficients on the host, the energy and the traces on the device (no
+    CPU fallback: raises without one)."""
+    c = kirkwood_coefficients(problem, n_terms)
+    q = problem.charges.charges
+    energy = _gpu_energy(c.units, q, c.reac, c.rpow, c.nmax) * (FOUR_PI * KCAL_MOL_PER_E2_ANG)
+    both = _gpu_traces(c.coef_phi, c.coef_dphi, c.units, c.rho, c.nmax)
+    return KirkwoodSolution(energy=energy, phi=lambda points: both(points)[0],
+                            dphi_dn=lambda points: both(points)[1], tail_ratio=c.tail_ratio,
+                            converged=c.tail_ratio <= 0.99, n_terms=n_terms)
 
 
 def kirkwood_centered(problem: SphereProblem):

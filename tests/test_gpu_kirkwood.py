@@ -1,6 +1,7 @@
 """f4 on the device: kirkwood_series' Legendre sums (csrc/hobi_kirkwood.cu)
 against the reference's own outputs (tests/golden/kirkwood.npz, made by
-pbbem.kirkwood.kirkwood_series) and against the host restatement."""
+pbbem.kirkwood.kirkwood_series) and against the numpy sums of
+oracle/kirkwood_host.py."""
 
 import ctypes as C
 
@@ -8,6 +9,7 @@ import numpy as np
 import pytest
 
 from conftest import golden
+from kirkwood_host import kirkwood_series_host
 from paper_1301_5914_b200 import ChargeSystem, PhysicalParams
 from paper_1301_5914_b200.kirkwood import SphereProblem, kirkwood_series
 
@@ -26,14 +28,14 @@ def _problem(g, tag):
 def test_device_series_matches_reference(tag):
     g = golden("kirkwood")
     sph, a = _problem(g, tag)
-    ks = kirkwood_series(sph, 40)  # backend="gpu" is the default
+    ks = kirkwood_series(sph, 40)
     assert ks.energy == pytest.approx(float(g[tag + "_energy"]), rel=1e-12)
     pts = a / 2.0 * g["points"]
     for name, fn in (("_phi", ks.phi), ("_dphi", ks.dphi_dn)):
         ref = g[tag + name]
         assert np.abs(fn(pts) - ref).max() <= 1e-12 * np.abs(ref).max(), name
     assert ks.converged == bool(g[tag + "_tail"][1])
-    host = kirkwood_series(sph, 40, backend="host")
+    host = kirkwood_series_host(sph, 40)
     assert abs(ks.energy - host.energy) <= 1e-13 * abs(host.energy)
     assert np.abs(ks.phi(pts) - host.phi(pts)).max() <= 1e-13 * np.abs(host.phi(pts)).max()
     assert ks.phi(pts[3]) == pytest.approx(ks.phi(pts)[3], rel=0, abs=0)  # single point
@@ -41,7 +43,7 @@ def test_device_series_matches_reference(tag):
 
 def test_device_series_many_points_and_charges():
     """Config-5-sized evaluation (L7 icosphere vertices, 200 charges): the device
-    sums agree with the host restatement everywhere."""
+    sums agree with the numpy sums everywhere."""
     from paper_1301_5914_b200.mesh import icosahedral_sphere
     from paper_1301_5914_b200.surfaces import sphere_charges
 
@@ -49,7 +51,7 @@ def test_device_series_many_points_and_charges():
     ch = sphere_charges(200, 1.2, 77)
     sph = SphereProblem(2.0, PhysicalParams(1.0, 80.0, 0.1257), ch)
     dev = kirkwood_series(sph, 40)
-    host = kirkwood_series(sph, 40, backend="host")
+    host = kirkwood_series_host(sph, 40)
     sub = pts[::97]
     for f, h in ((dev.phi, host.phi), (dev.dphi_dn, host.dphi_dn)):
         ref = h(sub)

@@ -1,13 +1,15 @@
 """Analytic Kirkwood validator against the reference's
-kirkwood_series / kirkwood_centered outputs (tests/golden/kirkwood.npz)."""
+kirkwood_series / kirkwood_centered outputs (tests/golden/kirkwood.npz): the
+product's host coefficients (kirkwood_coefficients) with the numpy Legendre
+sums of oracle/kirkwood_host.py; the device sums are tests/test_gpu_kirkwood.py."""
 
 import numpy as np
 import pytest
 
 from conftest import golden
 from paper_1301_5914_b200 import ChargeSystem, PhysicalParams
-from paper_1301_5914_b200.kirkwood import (NotCenteredError, SphereProblem, bessel_log_derivative,
-                                           kirkwood_centered, kirkwood_series, legendre_table)
+from kirkwood_host import kirkwood_series_host, legendre_table
+from paper_1301_5914_b200.kirkwood import NotCenteredError, SphereProblem, bessel_log_derivative, kirkwood_centered
 
 
 @pytest.mark.parametrize("tag", ["c2", "ecc", "lap"])
@@ -17,7 +19,7 @@ def test_series_matches_reference(tag):
     e1, e2, kap, a = v[-4:]
     nq = (v.size - 4) // 4
     pos, q = v[: 3 * nq].reshape(nq, 3), v[3 * nq: 4 * nq]
-    ks = kirkwood_series(SphereProblem(a, PhysicalParams(e1, e2, kap), ChargeSystem(pos, q)), 40, backend="host")
+    ks = kirkwood_series_host(SphereProblem(a, PhysicalParams(e1, e2, kap), ChargeSystem(pos, q)), 40)
     assert ks.energy == pytest.approx(float(g[tag + "_energy"]), rel=1e-12)
     pts = a / 2.0 * g["points"]
     for name, fn in (("_phi", ks.phi), ("_dphi", ks.dphi_dn)):
@@ -33,7 +35,7 @@ def test_centered_closed_form_and_series_agree():
     e, phi, dphi = kirkwood_centered(sph)
     assert np.allclose([e, phi(np.array([0, 0, 2.0])), dphi(np.array([0, 0, 2.0]))], g["centered"],
                        rtol=1e-14, atol=0)
-    ks = kirkwood_series(sph, 10, backend="host")
+    ks = kirkwood_series_host(sph, 10)
     assert ks.energy == pytest.approx(e, rel=1e-12)
     with pytest.raises(NotCenteredError):
         kirkwood_centered(SphereProblem(2.0, sph.params, ChargeSystem([[0, 0, 0.5]], [1.0])))
