@@ -1,4 +1,8 @@
 set -x
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2o_launch_list_c4.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-solve > gpurun_out/r2o_ncu_bench.log 2>&1
-python tools/launch_summary.py gpurun_out/r2o_launch_list_c4.csv > gpurun_out/r2o_launch_summary_c4.txt 2>&1
-timeout 1200 python bench.py --config 5 --steps 5 --warmup 3 > gpurun_out/r2o_bench_c5.json 2> gpurun_out/r2o_bench_c5.err
+for i in 1 2; do
+timeout 600 python bench.py --no-cpu-baseline --no-solve > gpurun_out/r2p_bench_default_$i.json 2> /dev/null
+cp paper_1301_5914_b200/libhobi.so /tmp/libhobi_default.so
+cp tools/_libhobi_O1.so paper_1301_5914_b200/libhobi.so
+timeout 600 python bench.py --no-cpu-baseline --no-solve > gpurun_out/r2p_bench_O1_$i.json 2> gpurun_out/r2p_bench_O1.err
+cp /tmp/libhobi_default.so paper_1301_5914_b200/libhobi.so
+done
