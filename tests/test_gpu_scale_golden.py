@@ -1,6 +1,6 @@
 """Parity at the BASELINE sizes against the reference itself.
 
-The fixtures (tests/golden/c3_solve.npz, c4_rows.npz, c5_rows.npz,
+The fixtures (tests/golden/c3_solve.npz, c4_solve.npz, c4_rows.npz, c5_rows.npz,
 c4_rows_lobi.npz (the LOBI scheme), made by
 tests/golden/make_scale_golden.py running unmodified pbbem in the build
 container) hold reference outputs for the seeded configs 3, 4 (the bench
@@ -67,11 +67,15 @@ def test_rows_match_reference_at_scale(index, scheme):
     prob.close()
 
 
-def test_config3_solve_matches_reference():
+@pytest.mark.parametrize("index", [3, 4])
+def test_solve_matches_reference(index):
+    """Configs 3 and 4 (the bench config) end to end against a full pbbem
+    solve: matvec, RHS, GMRES iteration and matvec counts, potentials and
+    energy."""
     from paper_1301_5914_b200 import assemble_rhs, gmres_solve, make_operator, matvec_hobi, solvation_energy
 
-    fx = _fixture("c3_solve")
-    cfg, scfg, prob = _problem(3, fx)
+    fx = _fixture(f"c{index}_solve")
+    cfg, scfg, prob = _problem(index, fx)
     nv = prob.n_collocation
     u = np.random.default_rng(int(fx["u_seed"])).standard_normal(2 * nv)
     assert rel_l2(matvec_hobi(prob, u), fx["Au"]) <= 1e-12
