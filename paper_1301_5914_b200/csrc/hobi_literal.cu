@@ -227,12 +227,9 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 int launch_singular(hobi_ctx* c, const double* u_dev, int64_t p0, int64_t p1, cudaStream_t stream) {
   if (p1 <= p0) return 0;
-  // HOBI_SINGULAR: "fast" (default, hobi_sweep.cu), "warp" (literal
-  // transcription, one warp per pair) or "serial" (literal, one thread per
-  // pair; HOBI_SINGULAR_SERIAL=1 is the older spelling)
+  // HOBI_SINGULAR: "fast" (default, hobi_singular.cu), "warp" (literal
+  // transcription, one warp per pair) or "serial" (literal, one thread per pair)
   static const int kind = [] {
-    const char* s = getenv("HOBI_SINGULAR_SERIAL");
-    if (s && s[0] == '1') return 2;
     const char* e = getenv("HOBI_SINGULAR");
     if (e && !strcmp(e, "serial")) return 2;
     if (e && !strcmp(e, "warp")) return 1;

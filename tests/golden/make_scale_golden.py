@@ -4,6 +4,7 @@ Run in the build container, where the reference is importable:
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_scale_golden.py c3 c4rows c5rows
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_scale_golden.py c4solve
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_scale_golden.py c4lobirows c5lobirows
 
 Every output array comes from the unmodified reference package ``pbbem``
 (``solver.discretize``, ``solver._apply_range`` -- the row-range unit its fork
@@ -131,7 +132,7 @@ def solve_case(index, workers=8, name=None):
 
 def main():
     jobs = {"c3": lambda: solve_case(3), "c4rows": lambda: rows_case(4), "c5rows": lambda: rows_case(5),
-            "c4lobirows": lambda: rows_case(4, scheme="lobi"),
+            "c4lobirows": lambda: rows_case(4, scheme="lobi"), "c5lobirows": lambda: rows_case(5, scheme="lobi"),
             "c4solve": lambda: solve_case(4, workers=int(os.environ.get("WORKERS", "6")))}
     for name in sys.argv[1:] or ["c3", "c4rows", "c5rows"]:
         jobs[name]()

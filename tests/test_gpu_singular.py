@@ -40,7 +40,6 @@ np.savez(sys.argv[1], **out)
 def _run(tmp_path, kind, variant=None):
     path = os.path.join(tmp_path, f"mv_{kind}_{variant}.npz")
     env = dict(os.environ, PYTHONPATH=ROOT)
-    env.pop("HOBI_SINGULAR_SERIAL", None)
     env.pop("HOBI_SINGULAR_VARIANT", None)
     env["HOBI_SINGULAR"] = kind
     if variant is not None:
