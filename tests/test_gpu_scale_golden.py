@@ -1,7 +1,7 @@
 """Parity at the BASELINE sizes against the reference itself.
 
 The fixtures (tests/golden/c3_solve.npz, c4_solve.npz, c4_rows.npz, c5_rows.npz,
-c4_rows_lobi.npz (the LOBI scheme), made by
+c4_rows_lobi.npz and c5_rows_lobi.npz (the LOBI scheme), made by
 tests/golden/make_scale_golden.py running unmodified pbbem in the build
 container) hold reference outputs for the seeded configs 3, 4 (the bench
 config) and 5; the meshes are regenerated here and checked against the
@@ -43,7 +43,7 @@ def _problem(index, fx, scheme="hobi"):
     return cfg, scfg, discretize(cfg.mesh, PhysicalParams(cfg.eps1, cfg.eps2, cfg.kappa), cfg.charges, scfg)
 
 
-@pytest.mark.parametrize("index,scheme", [(4, "hobi"), (5, "hobi"), (4, "lobi")])
+@pytest.mark.parametrize("index,scheme", [(4, "hobi"), (5, "hobi"), (4, "lobi"), (5, "lobi")])
 def test_rows_match_reference_at_scale(index, scheme):
     from paper_1301_5914_b200 import assemble_rhs, matvec_hobi, matvec_lobi
 

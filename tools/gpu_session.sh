@@ -1,2 +1,2 @@
 set -x
-timeout 900 python tests/checks/pbbem_solve_report.py 3 4 > gpurun_out/r2r_solve_report.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_scale_golden.py -q > gpurun_out/r2t_scale.txt 2>&1; echo "rc=$?" >> gpurun_out/r2t_scale.txt
