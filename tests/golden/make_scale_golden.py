@@ -93,13 +93,13 @@ def rows_case(index, workers=5, scheme="hobi"):
     print(f"c{index}rows ({scheme}): {time.time() - t0:.0f} s", flush=True)
 
 
-def solve_case(index, workers=8, name=None):
+def solve_case(index, workers=8, name=None, scheme="hobi"):
     t0 = time.time()
     cfg = baseline_config(index)
     nv = cfg.mesh.n_vertices
-    print(f"c{index}solve: N_v={nv} N_f={cfg.mesh.n_faces} workers={workers}", flush=True)
-    prob, scfg = _problem(cfg, workers)
-    u = np.random.default_rng(0).standard_normal(2 * nv)
+    print(f"c{index}solve ({scheme}): N_v={nv} N_f={cfg.mesh.n_faces} workers={workers}", flush=True)
+    prob, scfg = _problem(cfg, workers, scheme)
+    u = np.random.default_rng(0).standard_normal(2 * prob.n_collocation)
     count = [0]
     with rs.make_operator(prob, scfg) as op:
         t1 = time.time()
@@ -122,10 +122,11 @@ def solve_case(index, workers=8, name=None):
                Au=Au, rhs=rhs, phi=sol.phi, dphi=sol.dphi_dn, iterations=np.array(sol.iterations),
                residual=np.array(sol.residual), matvecs=np.array(count[0]), restart=np.array(cfg.restart),
                tol=np.array(cfg.tol), energy=np.array(energy),
-               params=np.array([cfg.eps1, cfg.eps2, cfg.kappa]),
+               params=np.array([cfg.eps1, cfg.eps2, cfg.kappa]), scheme=np.array(scheme),
                reference_solve_seconds=np.array(solve_s), reference_workers=np.array(workers),
                generated_by=np.array("pbbem make_operator/assemble_rhs/gmres_solve/solvation_energy"))
-    np.savez_compressed(os.path.join(HERE, name or f"c{index}_solve.npz"), **out)
+    tag = "" if scheme == "hobi" else "_" + scheme
+    np.savez_compressed(os.path.join(HERE, name or f"c{index}_solve{tag}.npz"), **out)
     print(f"c{index}solve: its={sol.iterations} matvecs={count[0]} E={energy!r} "
           f"solve {solve_s:.0f} s, total {time.time() - t0:.0f} s", flush=True)
 
@@ -133,7 +134,9 @@ def solve_case(index, workers=8, name=None):
 def main():
     jobs = {"c3": lambda: solve_case(3), "c4rows": lambda: rows_case(4), "c5rows": lambda: rows_case(5),
             "c4lobirows": lambda: rows_case(4, scheme="lobi"), "c5lobirows": lambda: rows_case(5, scheme="lobi"),
-            "c4solve": lambda: solve_case(4, workers=int(os.environ.get("WORKERS", "6")))}
+            "c4solve": lambda: solve_case(4, workers=int(os.environ.get("WORKERS", "6"))),
+            "c3lobisolve": lambda: solve_case(3, workers=int(os.environ.get("WORKERS", "6")), scheme="lobi"),
+            "c4lobisolve": lambda: solve_case(4, workers=int(os.environ.get("WORKERS", "6")), scheme="lobi")}
     for name in sys.argv[1:] or ["c3", "c4rows", "c5rows"]:
         jobs[name]()
 

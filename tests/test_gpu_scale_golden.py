@@ -67,18 +67,21 @@ def test_rows_match_reference_at_scale(index, scheme):
     prob.close()
 
 
-@pytest.mark.parametrize("index", [3, 4])
-def test_solve_matches_reference(index):
+@pytest.mark.parametrize("index,scheme", [(3, "hobi"), (4, "hobi"), (3, "lobi")])
+def test_solve_matches_reference(index, scheme):
     """Configs 3 and 4 (the bench config) end to end against a full pbbem
-    solve: matvec, RHS, GMRES iteration and matvec counts, potentials and
-    energy."""
-    from paper_1301_5914_b200 import assemble_rhs, gmres_solve, make_operator, matvec_hobi, solvation_energy
+    solve, both schemes: matvec, RHS, GMRES iteration and matvec counts,
+    potentials and energy."""
+    from paper_1301_5914_b200 import (assemble_rhs, gmres_solve, make_operator, matvec_hobi, matvec_lobi,
+                                      solvation_energy)
 
-    fx = _fixture(f"c{index}_solve")
-    cfg, scfg, prob = _problem(index, fx)
+    name = f"c{index}_solve" + ("" if scheme == "hobi" else "_" + scheme)
+    fx = _fixture(name)
+    assert str(fx.get("scheme", "hobi")) == scheme
+    cfg, scfg, prob = _problem(index, fx, scheme)
     nv = prob.n_collocation
     u = np.random.default_rng(int(fx["u_seed"])).standard_normal(2 * nv)
-    assert rel_l2(matvec_hobi(prob, u), fx["Au"]) <= 1e-12
+    assert rel_l2((matvec_hobi if scheme == "hobi" else matvec_lobi)(prob, u), fx["Au"]) <= 1e-12
     b = assemble_rhs(prob)
     assert rel_l2(b, fx["rhs"]) <= 1e-13
     with make_operator(prob, scfg) as op:

@@ -15,13 +15,16 @@ sys.path.insert(0, GOLDEN)
 
 
 @pytest.mark.parametrize("name,index", [("c3_solve", 3), ("c4_rows", 4), ("c5_rows", 5), ("c4_rows_lobi", 4),
-                                        ("c5_rows_lobi", 5), ("c4_solve", 4)])
+                                        ("c5_rows_lobi", 5), ("c4_solve", 4), ("c3_solve_lobi", 3),
+                                        ("c4_solve_lobi", 4)])
 def test_fixture_inputs_are_reproduced(name, index):
     from scale_hash import input_hash
 
     from paper_1301_5914_b200.surfaces import baseline_config
 
     path = os.path.join(GOLDEN, name + ".npz")
+    if name == "c4_solve_lobi" and not os.path.exists(path):
+        pytest.skip("config-4 LOBI pbbem solve fixture not generated yet")
     fx = np.load(path)
     cfg = baseline_config(index)
     assert input_hash(cfg) == str(fx["input_sha256"])

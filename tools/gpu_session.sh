@@ -1,3 +1,3 @@
 set -x
-timeout 1500 python tools/size_sweep.py > gpurun_out/r2u_size_sweep.md 2> gpurun_out/r2u_size_sweep.err
-timeout 900 python tools/solve_table.py 1 2 3 4 > gpurun_out/r2u_solve_table.jsonl 2> gpurun_out/r2u_solve_table.err
+timeout 900 python -m pytest tests/test_gpu_scale_golden.py -q -k "not 4-lobi" > gpurun_out/r2v_scale.txt 2>&1; echo "rc=$?" >> gpurun_out/r2v_scale.txt
+timeout 900 python tests/checks/pbbem_solve_report.py 3 4 3lobi > gpurun_out/r2v_solve_report.txt 2>&1
