@@ -173,6 +173,43 @@ int hobi_export_nodes(hobi_ctx* ctx, double* node_pos, double* node_nrm);
 int hobi_kernel_values(int device, const double* d, const double* nx, const double* ny, int64_t n,
                        double eps1, double eps2, double kappa, double* k);
 
+/* kernels.source_terms_at (kernels.py:159-178): S1 = sum_k q_k G0 and
+ * S2 = sum_k q_k dG0/dn_x at m surface points (m,3) with unit normals (m,3),
+ * unscaled.  HOBI_ERR_SINGULARITY ("surface point i coincides with charge k")
+ * when a point sits on a charge. */
+int hobi_source_terms(int device, const double* points, const double* normals, int64_t m,
+                      const double* qpos, const double* q, int64_t nc, double* s1, double* s2);
+
+/*
+ * The geometry module's functions (geometry.py) on caller arrays: the device
+ * functions the precompute of hobi_create runs, batched over n items.
+ *
+ * hobi_geometry_fit_arcs: fit_arc (geometry.py:46-84) for n endpoint pairs
+ *   (n,3) each; coef is (n, 4, 3) = c0..c3, code[i] is 0, 1 (endpoints
+ *   coincide) or 2 (endpoint normal nearly parallel to the chord).
+ * hobi_geometry_arc_normals: arc_normal (geometry.py:99-121) at parameter t[i]
+ *   of arc coef[i] with sign reference (n,3); straight[i] = 1 where the
+ *   reference itself was returned.
+ * hobi_geometry_nodes: nodes_from_vertex_data (geometry.py:261-302) for n
+ *   vertex triples, vertex_pos / vertex_nrm (n, 3, 3); node_pos / node_nrm are
+ *   (n, 10, 3).  first_bad = -1, or the first triple whose arcs are degenerate
+ *   with bad_code 1, 2 or 3 (endpoint normals antiparallel); the node arrays
+ *   are not written then.
+ * hobi_geometry_frames: frames_at (geometry.py:342-359) for n_elements
+ *   elements (n, 10, 3) at n_points reference points given as the (3,
+ *   n_points, 10) table N, dN/dr, dN/ds; pos / nrm are (n, n_points, 3), jac
+ *   (n, n_points); d_dr / d_ds (n, n_points, 3) may be NULL.
+ */
+int hobi_geometry_fit_arcs(int device, const double* p0, const double* n0, const double* p1,
+                           const double* n1, int64_t n, double* coef, int* code);
+int hobi_geometry_arc_normals(int device, const double* coef, const double* t, const double* reference,
+                              int64_t n, double* normals, int* straight);
+int hobi_geometry_nodes(int device, const double* vertex_pos, const double* vertex_nrm, int64_t n,
+                        double* node_pos, double* node_nrm, int64_t* first_bad, int* bad_code);
+int hobi_geometry_frames(int device, const double* node_pos, const double* node_nrm, int64_t n_elements,
+                         const double* shape, int n_points, double* pos, double* nrm, double* jac,
+                         double* d_dr, double* d_ds);
+
 /*
  * Multi-GPU row split: one process per GPU.  Rank r owns rows
  * partition_targets(n_colloc, nranks)[r] (solver.py:405-418); each matvec

@@ -72,6 +72,11 @@ SIGNATURES = {
     "hobi_export_nodes": (C.c_int, [_ctxp, _dp, _dp]),
     "hobi_kernel_values": (C.c_int, [C.c_int, _dp, _dp, _dp, C.c_int64, C.c_double, C.c_double,
                                      C.c_double, _dp]),
+    "hobi_source_terms": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _dp, _dp, C.c_int64, _dp, _dp]),
+    "hobi_geometry_fit_arcs": (C.c_int, [C.c_int, _dp, _dp, _dp, _dp, C.c_int64, _dp, C.POINTER(C.c_int)]),
+    "hobi_geometry_arc_normals": (C.c_int, [C.c_int, _dp, _dp, _dp, C.c_int64, _dp, C.POINTER(C.c_int)]),
+    "hobi_geometry_nodes": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _dp, _dp, _i64p, C.POINTER(C.c_int)]),
+    "hobi_geometry_frames": (C.c_int, [C.c_int, _dp, _dp, C.c_int64, _dp, C.c_int, _dp, _dp, _dp, _dp, _dp]),
     "hobi_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
     "hobi_comm_init": (C.c_int, [_ctxp, C.POINTER(C.c_ubyte), C.c_int, C.c_int]),
     "hobi_emulate_ranks": (C.c_int, [_ctxp, C.c_int]),

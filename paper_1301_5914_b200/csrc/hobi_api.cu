@@ -750,6 +750,50 @@ int hobi_kernel_values(int device, const double* d, const double* nx, const doub
   return kernel_values_device(d, nx, ny, n, eps1, eps2, kappa, k);
 }
 
+int hobi_source_terms(int device, const double* points, const double* normals, int64_t m,
+                      const double* qpos, const double* q, int64_t nc, double* s1, double* s2) {
+  if (m < 0 || nc < 0) return fail(HOBI_ERR_VALUE, "negative point or charge count");
+  if ((m && (!points || !normals || !s1 || !s2)) || (nc && (!qpos || !q)))
+    return fail(HOBI_ERR_VALUE, "null array");
+  HOBI_CUDA(cudaSetDevice(device));
+  return source_terms_device(points, normals, m, qpos, q, nc, s1, s2);
+}
+
+int hobi_geometry_fit_arcs(int device, const double* p0, const double* n0, const double* p1,
+                           const double* n1, int64_t n, double* coef, int* code) {
+  if (n < 0) return fail(HOBI_ERR_VALUE, "negative count");
+  if (n && (!p0 || !n0 || !p1 || !n1 || !coef || !code)) return fail(HOBI_ERR_VALUE, "null array");
+  HOBI_CUDA(cudaSetDevice(device));
+  return geometry_fit_arcs(p0, n0, p1, n1, n, coef, code);
+}
+
+int hobi_geometry_arc_normals(int device, const double* coef, const double* t, const double* reference,
+                              int64_t n, double* normals, int* straight) {
+  if (n < 0) return fail(HOBI_ERR_VALUE, "negative count");
+  if (n && (!coef || !t || !reference || !normals || !straight)) return fail(HOBI_ERR_VALUE, "null array");
+  HOBI_CUDA(cudaSetDevice(device));
+  return geometry_arc_normals(coef, t, reference, n, normals, straight);
+}
+
+int hobi_geometry_nodes(int device, const double* vertex_pos, const double* vertex_nrm, int64_t n,
+                        double* node_pos, double* node_nrm, int64_t* first_bad, int* bad_code) {
+  if (n < 0) return fail(HOBI_ERR_VALUE, "negative count");
+  if (!first_bad || !bad_code || (n && (!vertex_pos || !vertex_nrm || !node_pos || !node_nrm)))
+    return fail(HOBI_ERR_VALUE, "null array");
+  HOBI_CUDA(cudaSetDevice(device));
+  return geometry_nodes(vertex_pos, vertex_nrm, n, node_pos, node_nrm, first_bad, bad_code);
+}
+
+int hobi_geometry_frames(int device, const double* node_pos, const double* node_nrm, int64_t n_elements,
+                         const double* shape, int n_points, double* pos, double* nrm, double* jac,
+                         double* d_dr, double* d_ds) {
+  if (n_elements < 0 || n_points < 0) return fail(HOBI_ERR_VALUE, "negative count");
+  if (n_elements && n_points && (!node_pos || !node_nrm || !shape || !pos || !nrm || !jac))
+    return fail(HOBI_ERR_VALUE, "null array");
+  HOBI_CUDA(cudaSetDevice(device));
+  return geometry_frames(node_pos, node_nrm, n_elements, shape, n_points, pos, nrm, jac, d_dr, d_ds);
+}
+
 int hobi_comm_unique_id(unsigned char id[128]) {
   auto& a = nccl::api();
   if (!a.loaded) return fail(HOBI_ERR_NCCL, "libnccl.so.2 could not be loaded");

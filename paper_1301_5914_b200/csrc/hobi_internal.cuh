@@ -302,6 +302,15 @@ namespace hobi {
 int upload_rule_tables(const double* reg_shape, int nq, const double* duf_shape, int nd,
                        const double* reg_wts, const double* duf_wts);
 int build_geometry(hobi_ctx* c, const int* pair_of_slot, int* first_bad_slot, int* bad_code);
+// function-level geometry (geometry.py) on caller arrays, current device, default stream
+int geometry_fit_arcs(const double* p0, const double* n0, const double* p1, const double* n1, int64_t n,
+                      double* coef, int* code);
+int geometry_arc_normals(const double* coef, const double* t, const double* ref, int64_t n, double* nrm,
+                         int* straight);
+int geometry_nodes(const double* vdata, const double* ndata, int64_t n, double* node_pos,
+                   double* node_nrm, int64_t* first_bad, int* bad_code);
+int geometry_frames(const double* node_pos, const double* node_nrm, int64_t nelem, const double* shape,
+                    int m, double* pos, double* nrm, double* jac, double* d_dr, double* d_ds);
 
 // sweep (hobi_sweep.cu)
 int upload_exp_table();
@@ -320,6 +329,8 @@ int matvec_full_device(hobi_ctx* c, const double* u_dev, double* out_dev);
 int energy_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc,
                   const double* x_dev, double* energy);
 int rhs_device(hobi_ctx* c, const double* qpos, const double* q, int64_t nc, double* b_dev);
+int source_terms_device(const double* points, const double* normals, int64_t m, const double* qpos,
+                        const double* q, int64_t nc, double* s1, double* s2);
 int kernel_values_device(const double* d, const double* nx, const double* ny, int64_t n,
                          double eps1, double eps2, double kappa, double* k);
 

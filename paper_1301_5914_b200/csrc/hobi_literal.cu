@@ -335,4 +335,38 @@ int kernel_values_device(const double* d, const double* nx, const double* ny, in
   return 0;
 }
 
+// kernels.source_terms_at (kernels.py:159-178) at arbitrary surface points:
+// the RHS kernel with eps1 = 1 (x/1.0 is exact), on the default stream.
+int source_terms_device(const double* points, const double* normals, int64_t m, const double* qpos,
+                        const double* q, int64_t nc, double* s1, double* s2) {
+  if (m == 0) return 0;
+  if (nc == 0) {
+    memset(s1, 0, m * sizeof(double));
+    memset(s2, 0, m * sizeof(double));
+    return 0;
+  }
+  DevBuf<double> dp, dn, dqp, dq, ds;
+  DevBuf<unsigned long long> bad;
+  if (dp.alloc(3 * m) || dn.alloc(3 * m) || dqp.alloc(3 * nc) || dq.alloc(nc) || ds.alloc(2 * m) ||
+      bad.alloc(1))
+    return HOBI_ERR_CUDA;
+  HOBI_CUDA(cudaMemcpy(dp.p, points, 3 * m * sizeof(double), cudaMemcpyHostToDevice));
+  HOBI_CUDA(cudaMemcpy(dn.p, normals, 3 * m * sizeof(double), cudaMemcpyHostToDevice));
+  HOBI_CUDA(cudaMemcpy(dqp.p, qpos, 3 * nc * sizeof(double), cudaMemcpyHostToDevice));
+  HOBI_CUDA(cudaMemcpy(dq.p, q, nc * sizeof(double), cudaMemcpyHostToDevice));
+  HOBI_CUDA(cudaMemset(bad.p, 0xff, sizeof(unsigned long long)));
+  rhs_kernel<<<nblk(m, 256), 256>>>(dp.p, dn.p, 0, m, dqp.p, dq.p, nc, 1.0, ds.p, ds.p + m, bad.p);
+  HOBI_CUDA(cudaGetLastError());
+  unsigned long long badh = 0;
+  HOBI_CUDA(cudaMemcpy(&badh, bad.p, sizeof(badh), cudaMemcpyDeviceToHost));
+  if (badh != ~0ull) {
+    unsigned long long i = badh / (unsigned long long)(nc + 1), k = badh % (unsigned long long)(nc + 1);
+    return fail(HOBI_ERR_SINGULARITY, "surface point " + std::to_string(i) + " coincides with charge " +
+                                          std::to_string(k));
+  }
+  HOBI_CUDA(cudaMemcpy(s1, ds.p, m * sizeof(double), cudaMemcpyDeviceToHost));
+  HOBI_CUDA(cudaMemcpy(s2, ds.p + m, m * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 }  // namespace hobi

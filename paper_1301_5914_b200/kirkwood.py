@@ -50,6 +50,34 @@ class SphereProblem:
                                  f"inside the sphere of radius {self.radius}")
 
 
+def legendre_all(nmax: int, x) -> np.ndarray:
+    """P_0..P_nmax at x by the three-term recurrence, shape (nmax+1,) + x.shape
+    (kirkwood.py:59-71).  Host helper; the series sums run the same
+    recurrence on the device (csrc/hobi_kirkwood.cu)."""
+    x = np.asarray(x, dtype=float)
+    out = np.zeros((nmax + 1,) + x.shape)
+    out[0] = 1.0
+    if nmax >= 1:
+        out[1] = x
+    for n in range(1, nmax):
+        out[n + 1] = ((2 * n + 1) * x * out[n] - n * out[n - 1]) / (n + 1)
+    return out
+
+
+def modified_spherical_kn(nmax: int, x: float) -> np.ndarray:
+    """k_0..k_nmax at x > 0 with k_0 = exp(-x)/x, by the upward recurrence
+    k_{n+1} = k_{n-1} + (2n+1)/x k_n (stable upward; kirkwood.py:74-89)."""
+    if x <= 0.0:
+        raise ValueError(f"argument must be positive, got {x}")
+    out = np.empty(nmax + 1)
+    out[0] = np.exp(-x) / x
+    if nmax >= 1:
+        out[1] = out[0] * (1.0 + 1.0 / x)
+    for n in range(1, nmax):
+        out[n + 1] = out[n - 1] + ((2 * n + 1) / x) * out[n]
+    return out
+
+
 def bessel_log_derivative(nmax: int, x: float) -> np.ndarray:
     """x k_n'(x)/k_n(x), n = 0..nmax, through tau_n = k_n/k_{n-1} (never overflows);
     x = 0 is the Laplace limit -(n+1) (kirkwood.py:92-110)."""

@@ -24,24 +24,12 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
+from .geometry import CurvedElement, DegenerateArcError
 from .mesh import ChargeSystem, FlatMesh
 from .physics import FOUR_PI, KCAL_MOL_PER_E2_ANG, PhysicalParams, SingularityError
 from .quadrature import TriangleRule, barycentric, duffy_rule, gauss_radau_rule, shape_tables
 
 SCHEMES = ("hobi", "lobi")
-
-
-@dataclass(frozen=True)
-class CurvedElement:
-    """10-node cubic element: positions, unit normals, source vertex ids (geometry.py:212-230)."""
-
-    nodes: np.ndarray
-    node_normals: np.ndarray
-    vertex_ids: tuple
-
-
-class DegenerateArcError(ValueError):
-    """An edge arc could not be fitted (geometry.py:24-25)."""
 
 
 class GmresNonConvergence(RuntimeError):
