@@ -5,6 +5,7 @@ GMRES, energy, NCCL row split), behind the reference package's Python API
 C ABI: ``include/hobi.h``.
 """
 
+from . import geometry, kernels  # noqa: F401  (pbbem.geometry / pbbem.kernels on the device)
 from .mesh import (ChargeSystem, FlatMesh, MeshFormatError, MeshValidationError, flat_area,
                    icosahedral_sphere, parse_charges, parse_msms, radial_project, write_msms)
 from .physics import FOUR_PI, KCAL_MOL_PER_E2_ANG, PhysicalParams, SingularityError
