@@ -559,12 +559,67 @@ int hobi_matvec_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
   return matvec_full_device(c, u_dev, out_dev);
 }
 
+// Host-buffer application of a small problem: a latency-bound call (config 1:
+// 0.03 ms of kernels) spends more time in two pageable copies, five launches
+// and their gaps than in the sweep, so the whole call -- H2D from a pinned
+// staging vector, the matvec's kernels on their streams, D2H into a pinned
+// staging vector -- is captured once and replayed as one graph launch.  Same
+// kernels, same arguments, same order: results are bitwise those of the
+// plain path.  HOBI_MATVEC_GRAPH=0 turns it off.
+static const size_t kHostGraphBytes = 256 << 10;
+
+static bool host_graph_eligible(const hobi_ctx* c, size_t bytes) {
+  if (bytes > kHostGraphBytes || c->host_calls < 1) return false;  // first call: plain path (opt-ins, caches)
+  if (c->comm.nranks != 1 || c->comm.nccl || c->comm.p2p || c->comm.emulated) return false;
+  static const bool off = [] {
+    const char* e = getenv("HOBI_MATVEC_GRAPH");
+    return e && e[0] == '0';
+  }();
+  return !off;
+}
+
+static int matvec_host_graph(hobi_ctx* c, const double* u, double* out, size_t bytes) {
+  if (!c->host_in.p && (c->host_in.alloc(2 * c->nt) || c->host_out.alloc(2 * c->nt))) return HOBI_ERR_CUDA;
+  const uint64_t key = 1 ^ ((uint64_t)(c->sweep_variant + 1) << 48) ^ ((uint64_t)c->variant_pinned << 60);
+  if (!c->host_graph.exec || c->host_graph.key != key) {
+    c->host_graph.reset();
+    const bool saved_timing = c->timing;
+    const int64_t l0 = c->launches;
+    c->timing = false;  // no event pairs inside a capture
+    HOBI_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = cudaMemcpyAsync(c->u.p, c->host_in.p, bytes, cudaMemcpyHostToDevice, c->stream);
+    int rc = e == cudaSuccess ? matvec_full_device(c, c->u.p, c->out.p) : cuda_fail(e, "cudaMemcpyAsync");
+    if (!rc) {
+      e = cudaMemcpyAsync(c->host_out.p, c->out.p, bytes, cudaMemcpyDeviceToHost, c->stream);
+      if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync");
+    }
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &captured);  // always leave capture mode
+    c->timing = saved_timing;
+    c->host_graph.graph = captured;
+    c->host_graph.step_launches = c->launches - l0;
+    c->launches = l0;  // counted per replay instead
+    if (rc) return rc;
+    if (ce != cudaSuccess) return cuda_fail(ce, "matvec capture");
+    HOBI_CUDA(cudaGraphInstantiate(&c->host_graph.exec, captured, 0));
+    c->host_graph.key = key;
+  }
+  memcpy(c->host_in.p, u, bytes);
+  HOBI_CUDA(cudaGraphLaunch(c->host_graph.exec, c->stream));
+  c->launches += c->host_graph.step_launches;
+  HOBI_CUDA(cudaStreamSynchronize(c->stream));
+  memcpy(out, c->host_out.p, bytes);
+  return 0;
+}
+
 int hobi_matvec(hobi_ctx* c, const double* u, double* out) {
   NvtxRange nvtx_("hobi_matvec");
   if (!c) return fail(HOBI_ERR_STATE, "null context");
   HOBI_CUDA(cudaSetDevice(c->device));
   const size_t bytes = 2 * c->nt * sizeof(double);
   if (c->nt == 0) return 0;
+  if (host_graph_eligible(c, bytes)) return matvec_host_graph(c, u, out, bytes);
+  c->host_calls++;
   HOBI_CUDA(cudaMemcpyAsync(c->u.p, u, bytes, cudaMemcpyHostToDevice, c->stream));
   int rc = matvec_full_device(c, c->u.p, c->out.p);
   if (rc) return rc;

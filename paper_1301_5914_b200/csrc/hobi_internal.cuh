@@ -294,6 +294,11 @@ struct hobi_ctx {
   bool variant_pinned = false;  // set by hobi_sweep_variant: no small-problem switch
   hobi::GmresWorkspace gmres_ws;
   hobi::ChargeWorkspace charge_ws;
+  // Small host-buffer applications (hobi_matvec up to kHostGraphBytes): pinned
+  // staging vectors and one captured graph, H2D -> matvec -> D2H, replayed per call.
+  hobi::GraphHolder host_graph;
+  hobi::HostBuf<double> host_in, host_out;
+  int64_t host_calls = 0;
 };
 
 namespace hobi {

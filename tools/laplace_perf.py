@@ -1,5 +1,6 @@
 """Sweep throughput at kappa = 0 (Laplace instantiation) vs screened, config-4 surface."""
 import sys, ctypes as C, numpy as np
+import os; os.environ.setdefault("HOBI_MATVEC_GRAPH", "0")  # event-timed sweeps need the plain host path
 sys.path.insert(0, '.')
 from paper_1301_5914_b200 import _native as N, discretize, PhysicalParams, SolverConfig, matvec_hobi, matvec_lobi
 from paper_1301_5914_b200.surfaces import baseline_config

@@ -1,4 +1,5 @@
 import sys, ctypes as C, numpy as np
+import os; os.environ.setdefault("HOBI_MATVEC_GRAPH", "0")  # event-timed sweeps need the plain host path
 sys.path.insert(0, '.')
 from paper_1301_5914_b200 import _native as N, discretize, PhysicalParams, SolverConfig, matvec_lobi, matvec_hobi
 from paper_1301_5914_b200.surfaces import baseline_config

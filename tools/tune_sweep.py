@@ -1,5 +1,6 @@
 """Scratch: time every sweep variant on a config (device time of the sweep kernel)."""
 import sys, ctypes as C
+import os; os.environ.setdefault("HOBI_MATVEC_GRAPH", "0")  # event-timed sweeps need the plain host path
 import numpy as np
 sys.path.insert(0, '.')
 from paper_1301_5914_b200 import _native as N, discretize, PhysicalParams, SolverConfig, matvec_hobi
