@@ -31,6 +31,11 @@ class NotCenteredError(ValueError):
     """The closed form was asked about an eccentric or multi-charge system."""
 
 
+class SeriesDivergenceError(ValueError):
+    """The requested truncation cannot converge for this geometry (kirkwood.py:30-31;
+    part of the module's surface, raised by neither implementation)."""
+
+
 @dataclass(frozen=True)
 class SphereProblem:
     """Sphere of `radius` at the origin with strictly interior charges."""

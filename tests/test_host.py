@@ -173,3 +173,24 @@ def test_cli_restart_flag_is_honoured_even_at_100():
     assert _restart(7, None) == 7
     args = build_parser().parse_args(["solve", "--config", "4"])
     assert args.restart is None
+
+
+def test_module_surface_matches_the_reference_package():
+    """Every public name of every pbbem module (tests/golden/pbbem_api.json, read
+    from the reference sources by make_api_surface.py) exists in the same-named
+    module here: the drop-in surface, checked by name without a GPU."""
+    import importlib
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "pbbem_api.json")
+    with open(path) as fh:
+        api = json.load(fh)
+    assert set(api) == {"cli", "geometry", "kernels", "kirkwood", "mesh", "quadrature", "report", "solver"}
+    missing = {}
+    for module, names in api.items():
+        mod = importlib.import_module("paper_1301_5914_b200." + module)
+        gone = [n for n in names if not hasattr(mod, n)]
+        if gone:
+            missing[module] = gone
+    assert not missing, missing
