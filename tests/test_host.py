@@ -178,19 +178,40 @@ def test_cli_restart_flag_is_honoured_even_at_100():
 def test_module_surface_matches_the_reference_package():
     """Every public name of every pbbem module (tests/golden/pbbem_api.json, read
     from the reference sources by make_api_surface.py) exists in the same-named
-    module here: the drop-in surface, checked by name without a GPU."""
+    module here, every public function takes the reference's positional
+    parameters in the reference's order (extra trailing ones must have
+    defaults), and every record class has the reference's fields: the drop-in
+    surface, checked without a GPU."""
+    import dataclasses
     import importlib
+    import inspect
     import json
     import os
 
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "pbbem_api.json")
     with open(path) as fh:
         api = json.load(fh)
-    assert set(api) == {"cli", "geometry", "kernels", "kirkwood", "mesh", "quadrature", "report", "solver"}
-    missing = {}
-    for module, names in api.items():
+    assert set(api["names"]) == {"cli", "geometry", "kernels", "kirkwood", "mesh", "quadrature", "report",
+                                 "solver"}
+    problems = []
+    for module, names in api["names"].items():
         mod = importlib.import_module("paper_1301_5914_b200." + module)
-        gone = [n for n in names if not hasattr(mod, n)]
-        if gone:
-            missing[module] = gone
-    assert not missing, missing
+        problems += [f"{module}.{n} missing" for n in names if not hasattr(mod, n)]
+        for fn, ref in api["signatures"].get(module, {}).items():
+            params = [p for p in inspect.signature(getattr(mod, fn)).parameters.values()
+                      if p.kind in (p.POSITIONAL_ONLY, p.POSITIONAL_OR_KEYWORD)]
+            if [p.name for p in params[:len(ref)]] != ref:
+                problems.append(f"{module}.{fn}{[p.name for p in params]} != {ref}")
+            problems += [f"{module}.{fn}: extra parameter {p.name} has no default" for p in params[len(ref):]
+                         if p.default is inspect.Parameter.empty]
+        for cls, ref in api["fields"].get(module, {}).items():
+            ours = getattr(mod, cls)
+            if dataclasses.is_dataclass(ours):
+                have = [f.name for f in dataclasses.fields(ours)]
+                if have[:len(ref)] != ref:
+                    problems.append(f"{module}.{cls} fields {have} != {ref}")
+            else:  # DiscretizedProblem: device-backed, caches exported on first access
+                src = inspect.getsource(ours)
+                problems += [f"{module}.{cls}.{f} missing" for f in ref
+                             if not (hasattr(ours, f) or f"self.{f}" in src or f'"{f}"' in src)]
+    assert not problems, problems
