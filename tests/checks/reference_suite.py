@@ -10,6 +10,7 @@ GPU box with the snapshot; the run itself reads only that staged copy.
     python tests/checks/reference_suite.py --stage          # build container
     gpurun -- python tests/checks/reference_suite.py        # GPU box
     python tests/checks/reference_suite.py -- -k kirkwood   # extra pytest args after --
+    python tests/checks/reference_suite.py --scripts        # the reference's scripts/ instead of its tests
 
 Prints pytest's per-file counts and one JSON summary line; exit code = pytest's.
 """
@@ -29,6 +30,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 STAGED = os.path.join(ROOT, "baseline", "_ref", "tests_pbbem")
 SOURCE = "/root/reference/pkg/tests"
+STAGED_SCRIPTS = os.path.join(ROOT, "baseline", "_ref", "scripts_pbbem")
+SOURCE_SCRIPTS = "/root/reference/pkg/scripts"
+# reference scripts (unmodified) and the arguments of the runs recorded in profiles/r02_reference_suite.md
+SCRIPT_RUNS = (("sphere_convergence.py", ["--levels", "1", "2", "3"]),
+               ("sphere_convergence.py", ["--eccentric", "--levels", "2", "3", "4"]),
+               ("worker_scaling.py", ["--level", "2", "--workers", "1", "2", "4"]))
 
 
 def stage() -> int:
@@ -38,12 +45,36 @@ def stage() -> int:
     shutil.rmtree(STAGED, ignore_errors=True)
     shutil.copytree(SOURCE, STAGED, ignore=shutil.ignore_patterns("__pycache__", ".hypothesis"))
     print(f"staged {len(os.listdir(STAGED))} files into {os.path.relpath(STAGED, ROOT)}")
+    shutil.rmtree(STAGED_SCRIPTS, ignore_errors=True)
+    shutil.copytree(SOURCE_SCRIPTS, STAGED_SCRIPTS, ignore=shutil.ignore_patterns("__pycache__"))
+    print(f"staged {len(os.listdir(STAGED_SCRIPTS))} files into {os.path.relpath(STAGED_SCRIPTS, ROOT)}")
     return 0
+
+
+def run_scripts() -> int:
+    """The reference's scripts/, files untouched, with pbbem aliased to this package."""
+    if not os.path.isdir(STAGED_SCRIPTS):
+        print(f"{STAGED_SCRIPTS} missing: run with --stage in the build container first", file=sys.stderr)
+        return 2
+    env = dict(os.environ)
+    env["PYTHONPATH"] = HERE + os.pathsep + ROOT + os.pathsep + env.get("PYTHONPATH", "")
+    worst = 0
+    for name, argv in SCRIPT_RUNS:
+        path = os.path.join(STAGED_SCRIPTS, name)
+        code = ("import sys, runpy, warnings; warnings.simplefilter('ignore'); import pbbem_alias; "
+                f"sys.argv = {[path] + argv!r}; runpy.run_path({path!r}, run_name='__main__')")
+        print(f"$ {name} {' '.join(argv)}", flush=True)
+        proc = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        print(proc.stdout + proc.stderr[-3000:], flush=True)
+        worst = max(worst, proc.returncode)
+    return worst
 
 
 def main(argv) -> int:
     if "--stage" in argv:
         return stage()
+    if "--scripts" in argv:
+        return run_scripts()
     extra = argv[argv.index("--") + 1:] if "--" in argv else []
     if not os.path.isdir(STAGED):
         print(f"{STAGED} missing: run with --stage in the build container first", file=sys.stderr)
