@@ -56,6 +56,7 @@ def _iptr(a: np.ndarray):
 
 def fit_arc(p0, n0, p1, n1, device: int = 0) -> CubicArc:
     """Cubic arc between two surface points with outward unit normals."""
+    N.require_device()
     coef = np.empty((1, 4, 3))
     code = np.zeros(1, dtype=np.intc)
     N.check(N.load().hobi_geometry_fit_arcs(device, N.dptr(_row(p0)), N.dptr(_row(n0)), N.dptr(_row(p1)),
@@ -80,6 +81,7 @@ def arc_acceleration(arc: CubicArc, t: float) -> np.ndarray:
 def arc_normal(arc: CubicArc, t: float, reference, device: int = 0):
     """(unit normal from the arc's curvature, signed like `reference`; True
     where the arc is locally straight and `reference` itself comes back)."""
+    N.require_device()
     coef = N.f64(np.stack([arc.c0, arc.c1, arc.c2, arc.c3]).reshape(1, 4, 3))
     tt = N.f64(np.array([t], dtype=float))
     out = np.empty((1, 3))
@@ -159,6 +161,7 @@ def nodes_for_triangles(vertex_pos, vertex_nrm, device: int = 0):
     """Batched nodes_from_vertex_data: (n, 3, 3) vertex positions and normals
     -> (n, 10, 3) node positions and normals, plus (first degenerate triple or
     -1, its message)."""
+    N.require_device()
     vp = N.f64(np.asarray(vertex_pos, dtype=float).reshape(-1, 3, 3))
     vn = N.f64(np.asarray(vertex_nrm, dtype=float).reshape(-1, 3, 3))
     n = vp.shape[0]
@@ -192,6 +195,7 @@ def build_curved_element(mesh: FlatMesh, face_index: int) -> CurvedElement:
 
 
 def _frames(node_pos, node_nrm, pts, tangents: bool, device: int = 0):
+    N.require_device()
     node_pos = N.f64(np.asarray(node_pos, dtype=float).reshape(-1, 10, 3))
     node_nrm = N.f64(np.asarray(node_nrm, dtype=float).reshape(-1, 10, 3))
     pts = np.asarray(pts, dtype=float).reshape(-1, 2)

@@ -55,6 +55,7 @@ def kernel_values_d(d, nx, ny, params: PhysicalParams, device: int = 0):
     n = int(np.prod(shape, dtype=np.int64))
     k = np.empty((4, n))
     if n:
+        N.require_device()
         dd, dx, dy = (N.f64(a.reshape(n, 3)) for a in (d, nx, ny))
         N.check(N.load().hobi_kernel_values(device, N.dptr(dd), N.dptr(dx), N.dptr(dy), n,
                                             params.eps1, params.eps2, params.kappa, N.dptr(k)))
@@ -85,6 +86,7 @@ def source_terms_at(points, normals, charges: ChargeSystem, device: int = 0):
     nc = len(charges)
     if m == 0 or nc == 0:
         return s1, s2
+    N.require_device()
     qpos, q = N.f64(charges.positions), N.f64(charges.charges)
     try:
         N.check(N.load().hobi_source_terms(device, N.dptr(points), N.dptr(normals), m, N.dptr(qpos),

@@ -88,6 +88,15 @@ def test_no_cpu_fallback_without_device():
                    SolverConfig())
     with pytest.raises(RuntimeError, match="CUDA device"):
         gmres_solve(lambda v: v, np.ones(4), SolverConfig())
+    from paper_1301_5914_b200 import geometry, kernels
+
+    for call in (lambda: geometry.fit_arc([1, 0, 0], [1, 0, 0], [0, 1, 0], [0, 1, 0]),
+                 lambda: geometry.frames_at(np.zeros((1, 10, 3)), np.zeros((1, 10, 3)), [[0.2, 0.2]]),
+                 lambda: geometry.nodes_from_vertex_data(*np.eye(3).repeat(2, axis=0)),
+                 lambda: kernels.kernel_values_d([1.0, 0, 0], [1.0, 0, 0], [0, 1.0, 0], PhysicalParams(1, 80, 0.1)),
+                 lambda: kernels.source_terms([1.0, 0, 0], [1.0, 0, 0], ChargeSystem([[0, 0, 0]], [1.0]))):
+        with pytest.raises(RuntimeError, match="CUDA device"):
+            call()
 
 
 def test_product_never_imports_the_oracle():
