@@ -569,7 +569,7 @@ int hobi_matvec_device(hobi_ctx* c, const double* u_dev, double* out_dev) {
 static const size_t kHostGraphBytes = 256 << 10;
 
 static bool host_graph_eligible(const hobi_ctx* c, size_t bytes) {
-  if (bytes > kHostGraphBytes || c->host_calls < 1) return false;  // first call: plain path (opt-ins, caches)
+  if (bytes > kHostGraphBytes || c->host_calls < 1 || c->host_graph_off) return false;  // first call: plain path
   if (c->comm.nranks != 1 || c->comm.nccl || c->comm.p2p || c->comm.emulated) return false;
   static const bool off = [] {
     const char* e = getenv("HOBI_MATVEC_GRAPH");
@@ -599,9 +599,15 @@ static int matvec_host_graph(hobi_ctx* c, const double* u, double* out, size_t b
     c->host_graph.graph = captured;
     c->host_graph.step_launches = c->launches - l0;
     c->launches = l0;  // counted per replay instead
-    if (rc) return rc;
-    if (ce != cudaSuccess) return cuda_fail(ce, "matvec capture");
-    HOBI_CUDA(cudaGraphInstantiate(&c->host_graph.exec, captured, 0));
+    cudaError_t ie = cudaSuccess;
+    if (!rc && ce == cudaSuccess) ie = cudaGraphInstantiate(&c->host_graph.exec, captured, 0);
+    if (rc || ce != cudaSuccess || ie != cudaSuccess) {
+      // not fatal: this context applies through the plain path from now on
+      c->host_graph.reset();
+      c->host_graph_off = true;
+      cudaGetLastError();
+      return hobi_matvec(c, u, out);
+    }
     c->host_graph.key = key;
   }
   memcpy(c->host_in.p, u, bytes);

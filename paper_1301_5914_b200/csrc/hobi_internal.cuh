@@ -299,6 +299,7 @@ struct hobi_ctx {
   hobi::GraphHolder host_graph;
   hobi::HostBuf<double> host_in, host_out;
   int64_t host_calls = 0;
+  bool host_graph_off = false;  // a capture failed once: this context keeps the plain path
 };
 
 namespace hobi {
