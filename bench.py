@@ -596,19 +596,22 @@ def run_ours(a):
     # --- solve through the public API ------------------------------------------
     solve = None
     if not a.no_solve:
-        barrier()
-        t0 = time.perf_counter()
-        b = assemble_rhs(prob)
-        op = run.op(make_operator, scfg)
-        sol = gmres_solve(op, b, scfg)
-        if op is not getattr(run, "group_op", None):
-            op.close()
-        energy = solvation_energy(prob, sol)
-        barrier()
-        dt = max_over_ranks(time.perf_counter() - t0)
-        solve = {"seconds": dt, "iterations": sol.iterations, "matvecs": sol.matvecs,
-                 "residual": sol.residual, "energy_kcal_mol": energy,
-                 "includes": "rhs + GMRES(restart %d, tol %g) + energy, wall clock" % (cfg.restart, cfg.tol)}
+        times = []
+        for _ in range(2):  # the first solve of a process also pays one-time allocations and graph capture
+            barrier()
+            t0 = time.perf_counter()
+            b = assemble_rhs(prob)
+            op = run.op(make_operator, scfg)
+            sol = gmres_solve(op, b, scfg)
+            if op is not getattr(run, "group_op", None):
+                op.close()
+            energy = solvation_energy(prob, sol)
+            barrier()
+            times.append(max_over_ranks(time.perf_counter() - t0))
+        solve = {"seconds": times[1], "first_seconds": times[0], "iterations": sol.iterations,
+                 "matvecs": sol.matvecs, "residual": sol.residual, "energy_kcal_mol": energy,
+                 "includes": "rhs + GMRES(restart %d, tol %g) + energy, wall clock; second of two solves "
+                             "(first_seconds: the process's first)" % (cfg.restart, cfg.tol)}
 
     # one-GPU model of the p-way row split: the slowest of the first and last
     # rank's compute (everything before the gather), device-timed; labelled a

@@ -37,7 +37,7 @@
 
 namespace hobi {
 
-__device__ double g_exp_table[kExpTable];
+__device__ __align__(128) double g_exp_table[kExpTable];  // 16-byte aligned for the bulk copy
 
 // Once per device (the table never changes; a sweep running in another
 // context reads it, so it is not rewritten under it).
@@ -67,8 +67,9 @@ const double* exp_table_device() {
 namespace {
 
 constexpr uint32_t kTileBytes = kSrcTile * kSrcStride * sizeof(double);
+constexpr uint32_t kExpBytes = kExpTable * sizeof(double);
 constexpr size_t kSweepSmem =
-    (size_t)kStages * kTileBytes + kExpTable * sizeof(double) + kStages * sizeof(uint64_t);
+    (size_t)kStages * kTileBytes + kExpBytes + (kStages + 1) * sizeof(uint64_t);  // ring, exp table, barriers
 
 // Persistent, dynamically scheduled sweep.  Work item = (target tile, source
 // group); items are numbered group-major so CTAs running concurrently share a
@@ -92,18 +93,40 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
   const int n_ttiles = (int)((t_end - t_begin + kTile - 1) / kTile);
   const int n_items = n_ttiles * n_groups;
 
-  if (MODE == kScreened)
+  // The 128-row tile (R == 1) serves small problems and remainder rows, where a
+  // CTA runs one or two 64-source items and its start-up is on the critical
+  // path (profiles/r02_small_sweep.md): there the exp table arrives by one
+  // bulk copy behind its own barrier instead of 16 loads and stores per
+  // thread, and the first item is the CTA's own index, so no CTA waits on a
+  // ticket round trip before its first tile (nor after its last one when the
+  // grid covers every item).  The wide tiles keep the plain prologue: their
+  // start-up is amortised over hundreds of tiles, and ptxas schedules their
+  // loop measurably worse next to the other prologue (same file).
+  constexpr bool kLean = R == 1;
+  if (!kLean && MODE == kScreened)
     for (int i = threadIdx.x; i < kExpTable; i += kSweepThreads) etab[i] = g_exp_table[i];
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages + (kLean ? 1 : 0); ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (kLean && MODE == kScreened) {
+      mbar_expect_tx(&bars[kStages], kExpBytes);
+      bulk_g2s(etab, g_exp_table, kExpBytes, &bars[kStages]);
+    }
   }
+  bool etab_pending = kLean && MODE == kScreened;
   uint32_t seq = 0;  // source tiles consumed so far by this CTA (ring position)
-  for (;;) {
-    if (threadIdx.x == 0) item_sh = (int)atomicAdd(ticket, 1u);
-    __syncthreads();
-    const int item = item_sh;
-    __syncthreads();
+  for (int pass = 0;; ++pass) {
+    int item;
+    if (kLean && pass == 0) {
+      item = (int)blockIdx.x;
+      __syncthreads();  // barriers initialised
+    } else {
+      if (kLean && (int)gridDim.x >= n_items) break;  // one item per CTA: nothing left to hand out
+      if (threadIdx.x == 0) item_sh = (kLean ? (int)gridDim.x : 0) + (int)atomicAdd(ticket, 1u);
+      __syncthreads();
+      item = item_sh;
+      __syncthreads();
+    }
     if (item >= n_items) break;
     const int g = item / n_ttiles;
     const int tt = item - g * n_ttiles;
@@ -135,6 +158,10 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) sweep_kernel(
       ny[q] = tgt[4 * ldt + t];
       a1[q] = 0.0;
       a2[q] = 0.0;
+    }
+    if (kLean && etab_pending) {  // first item only: the table's bulk copy has landed
+      mbar_wait(&bars[kStages], 0u);
+      etab_pending = false;
     }
     for (int it = 0; it < ntl; ++it) {
       if (threadIdx.x == 0 && it + kStages - 1 < ntl) {
