@@ -568,7 +568,7 @@ static const SweepVariant kVariants[] = {
     HOBI_V(4, 4, 2), HOBI_V(5, 3, 1), HOBI_VS(6, 2, 1), HOBI_VS(4, 3, 1), HOBI_VS(3, 4, 1),
     HOBI_VS(4, 3, 2), HOBI_VS(4, 3, 4), HOBI_VS(6, 2, 2), HOBI_VS(3, 4, 2), HOBI_VS(5, 3, 2),
     HOBI_VS(8, 2, 2), HOBI_VS(6, 2, 3), HOBI_VS(7, 2, 3), HOBI_V(1, 8, 4), HOBI_V(1, 8, 8),
-    HOBI_V(1, 6, 4),
+    HOBI_V(1, 6, 4), HOBI_V(1, 4, 8), HOBI_V(1, 5, 6), HOBI_V(1, 3, 12),
 };
 #undef HOBI_V
 #undef HOBI_VS
@@ -577,35 +577,37 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 static const SweepVariant kSelfVariants[] = {
     {sweep_kernel<kScreened, true, true, 7, 2, 3, true>, 7, "self_step_R7_minb2_unroll3"},
     {sweep_kernel<kScreened, true, true, 4, 3, 2, true>, 4, "self_step_R4_minb3_unroll2"},
-    {sweep_kernel<kScreened, true, true, 1, 6, 2>, 1, "self_R1_minb6_unroll2"},
+    {sweep_kernel<kScreened, true, true, 1, 3, 12>, 1, "self_R1_minb3_unroll12"},
 };
 // kappa = 0 (Laplace instantiation, no step-major form needed): wide / narrow
 // / small tiles, without and with the LOBI self mask.
 static const SweepVariant kLaplaceVariants[] = {
     {sweep_kernel<kLaplace, true, false, 7, 2, 3>, 7, "laplace_R7_minb2_unroll3"},
     {sweep_kernel<kLaplace, true, false, 4, 3, 2>, 4, "laplace_R4_minb3_unroll2"},
-    {sweep_kernel<kLaplace, true, false, 1, 8, 2>, 1, "laplace_R1_minb8_unroll2"},
+    {sweep_kernel<kLaplace, true, false, 1, 3, 12>, 1, "laplace_R1_minb3_unroll12"},
 };
 // energy sweeps (K1/K2 only, charges as targets), screened and kappa = 0
 static const SweepVariant kEnergyVariants[] = {
     {sweep_kernel<kScreened, false, false, 7, 2, 3>, 7, "energy_R7_minb2_unroll3"},
     {sweep_kernel<kScreened, false, false, 4, 3, 2>, 4, "energy_R4_minb3_unroll2"},
-    {sweep_kernel<kScreened, false, false, 1, 8, 2>, 1, "energy_R1_minb8_unroll2"},
+    {sweep_kernel<kScreened, false, false, 1, 3, 12>, 1, "energy_R1_minb3_unroll12"},
 };
 static const SweepVariant kEnergyLaplaceVariants[] = {
     {sweep_kernel<kLaplace, false, false, 7, 2, 3>, 7, "energy_laplace_R7_minb2_unroll3"},
     {sweep_kernel<kLaplace, false, false, 4, 3, 2>, 4, "energy_laplace_R4_minb3_unroll2"},
-    {sweep_kernel<kLaplace, false, false, 1, 8, 2>, 1, "energy_laplace_R1_minb8_unroll2"},
+    {sweep_kernel<kLaplace, false, false, 1, 3, 12>, 1, "energy_laplace_R1_minb3_unroll12"},
 };
 static const SweepVariant kLaplaceSelfVariants[] = {
     {sweep_kernel<kLaplace, true, true, 7, 2, 3>, 7, "laplace_self_R7_minb2_unroll3"},
     {sweep_kernel<kLaplace, true, true, 4, 3, 2>, 4, "laplace_self_R4_minb3_unroll2"},
-    {sweep_kernel<kLaplace, true, true, 1, 6, 2>, 1, "laplace_self_R1_minb6_unroll2"},
+    {sweep_kernel<kLaplace, true, true, 1, 3, 12>, 1, "laplace_self_R1_minb3_unroll12"},
 };
-// R1_minb8_unroll4: 128-row tiles with four sources in flight per thread
-// (config 1: 0.032 vs 0.039 ms for unroll 2, config 2: 0.192 vs 0.197 ms,
-// profiles/r02_small_configs.md)
-constexpr int kSmallVariant = 23;
+// R1_minb3_unroll12: 128-row tiles with twelve sources in flight per thread
+// (112 registers): the 128-row tile runs with few warps per SM, so its FP64
+// dependence chains need the instruction-level parallelism (config 1: 0.026 ms
+// vs 0.030 for unroll 4 and 0.039 for unroll 2; pinned on config 4: 38.9 vs
+// 39.7 ms; profiles/r02_small_configs.md)
+constexpr int kSmallVariant = 28;
 constexpr int kWideVariant = 22;   // step_R7_minb2_unroll3: 896-row tiles, the default
 constexpr int kNarrowVariant = 15; // step_R4_minb3_unroll2: 512-row tiles
 static_assert(kWideVariant < kNumVariants && kNarrowVariant < kNumVariants && kSmallVariant < kNumVariants,
