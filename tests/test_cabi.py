@@ -193,4 +193,19 @@ def test_round2_entry_points_validate_arguments_without_a_device():
     ms = np.zeros(1)
     assert lib.hobi_group_bench(None, N.dptr(z), N.dptr(z), 1, 0, 0, N.dptr(ms)) == N.HOBI_ERR_STATE
     assert "null" in N.last_error()
-    del C
+    # the function-level geometry / kernels entries: sizes and null arrays first
+    ci = (C.c_int * 1)()
+    bad, code = (C.c_int64 * 1)(), (C.c_int * 1)()
+    assert lib.hobi_geometry_fit_arcs(0, N.dptr(z), N.dptr(z), N.dptr(z), N.dptr(z), -1, N.dptr(z), ci) == N.HOBI_ERR_VALUE
+    assert lib.hobi_geometry_fit_arcs(0, None, N.dptr(z), N.dptr(z), N.dptr(z), 1, N.dptr(z), ci) == N.HOBI_ERR_VALUE
+    assert lib.hobi_geometry_arc_normals(0, N.dptr(z), None, N.dptr(z), 1, N.dptr(z), ci) == N.HOBI_ERR_VALUE
+    assert lib.hobi_geometry_nodes(0, N.dptr(z), N.dptr(z), 1, N.dptr(z), N.dptr(z), None, code) == N.HOBI_ERR_VALUE
+    assert lib.hobi_geometry_nodes(0, None, N.dptr(z), 1, N.dptr(z), N.dptr(z), bad, code) == N.HOBI_ERR_VALUE
+    assert lib.hobi_geometry_frames(0, N.dptr(z), N.dptr(z), 1, None, 2, N.dptr(z), N.dptr(z), N.dptr(z), None,
+                                    None) == N.HOBI_ERR_VALUE
+    assert lib.hobi_geometry_frames(0, N.dptr(z), N.dptr(z), -1, N.dptr(z), 2, N.dptr(z), N.dptr(z), N.dptr(z),
+                                    None, None) == N.HOBI_ERR_VALUE
+    assert lib.hobi_source_terms(0, N.dptr(z), N.dptr(z), -1, N.dptr(z), N.dptr(z), 1, N.dptr(z),
+                                 N.dptr(z)) == N.HOBI_ERR_VALUE
+    assert lib.hobi_source_terms(0, N.dptr(z), N.dptr(z), 1, None, N.dptr(z), 1, N.dptr(z),
+                                 N.dptr(z)) == N.HOBI_ERR_VALUE
